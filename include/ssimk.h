@@ -1,0 +1,179 @@
+/*
+ * ssimk.h — C ABI of the B200-native SSIM engine (libssimk.so).
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `ssimkit` (arXiv 2101.06354, /root/reference/pkg/src/ssimkit).  The reference
+ * has no FFI: its only dispatch seam is the `engine` string of
+ * `local_statistics` (src/stats.py:205-261, engine resolution :223-228).  Each
+ * entry point below replaces one numpy routine on that path; the replaced
+ * reference code is cited beside it.  INTEGRATION.md shows the ctypes binding
+ * a ssimkit maintainer would add behind that seam.
+ *
+ * Conventions
+ *  - Every pointer named `d_*` (and every pointer inside ssk_planes) is a
+ *    DEVICE pointer owned by the caller; nothing is allocated inside a call.
+ *    Scratch comes from a caller-provided workspace sized by the matching
+ *    *_workspace_bytes query.
+ *  - Calls are asynchronous on `stream` (a cudaStream_t / CUstream passed as
+ *    void*; NULL = legacy default stream) and re-entrant (no global mutable
+ *    state apart from a monotonically increasing launch counter).
+ *  - Return value: 0 on success, a negative SSK_E* code otherwise
+ *    (ssk_strerror gives the text).  Argument errors are detected before any
+ *    launch; the Python layer maps them onto the reference's exception classes
+ *    (src/errors.py).
+ *  - Geometry follows the reference exactly (valid region only, anchor (0,0),
+ *    window cell (r,c) covers rows [r*s, r*s+k) and cols [c*s, c*s+k);
+ *    grid = ((H-k)//s + 1, (W-k)//s + 1); src/stats.py:130-164).
+ */
+#ifndef SSIMK_H
+#define SSIMK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSK_ABI_VERSION 1
+
+/* sample storage types */
+enum {
+  SSK_U8 = 1,  /* uint8  samples (8-bit luma)                               */
+  SSK_U16 = 2, /* uint16 samples (9..16-bit luma, or a scaled pyramid level) */
+  SSK_U32 = 3, /* uint32 samples (scaled pyramid levels of deep inputs)      */
+  SSK_F32 = 4, /* float32 samples                                           */
+  SSK_F64 = 5  /* float64 samples (downsample only)                         */
+};
+
+/* window shapes (WindowSpec.shape, src/config.py:31-75) */
+enum { SSK_RECT = 1, SSK_GAUSS = 2 };
+
+/* what a scoring call produces */
+enum {
+  SSK_WANT_Q = 1,      /* per-frame sum of q = l*cs                           */
+  SSK_WANT_L = 2,      /* per-frame sum of l                                  */
+  SSK_WANT_CS = 4,     /* per-frame sum of cs                                 */
+  SSK_MAP_TERMS = 8,   /* write the l, cs, q maps (3 planes per frame)        */
+  SSK_MAP_STATS = 16   /* write mu1, mu2, var1, var2, cov (5 planes per frame) */
+};
+
+/* error codes */
+enum {
+  SSK_OK = 0,
+  SSK_E_ARG = -1,          /* bad argument (null pointer, bad enum, bad size)   */
+  SSK_E_WINDOW = -2,       /* window larger than the image                      */
+  SSK_E_SHAPE = -3,        /* unsupported window/engine combination             */
+  SSK_E_WORKSPACE = -4,    /* workspace too small                               */
+  SSK_E_ALIGN = -5,        /* base pointer / pitch not 16-byte aligned          */
+  SSK_E_CUDA = -6,         /* CUDA launch or runtime error                      */
+  SSK_E_LEVELS = -7,       /* too many scales for the image (TooManyLevels)     */
+  SSK_E_TOO_SMALL = -8     /* cannot downsample (TooSmall)                      */
+};
+
+/*
+ * A batch of n reference/distorted frame pairs of identical geometry.
+ * Pointers must be 16-byte aligned and row_pitch*sizeof(sample) a multiple
+ * of 16 (the Python layer pads when a caller's tensor is not).
+ * Sample value = stored value * 2^-scale_log2 (scale_log2 = 2*s for a scaled
+ * integer pyramid level s, whose stored values are sums of 4^s samples).
+ */
+typedef struct ssk_planes {
+  const void* ref;
+  const void* dist;
+  int32_t dtype;        /* SSK_U8 / SSK_U16 / SSK_U32 / SSK_F32             */
+  int32_t scale_log2;   /* 0 for ordinary planes                            */
+  int32_t n, h, w;      /* frames, rows, columns                            */
+  int32_t bit_depth;    /* of the source samples (8..16); selects shift L/2 */
+  int64_t row_pitch;    /* elements between rows                            */
+  int64_t frame_pitch;  /* elements between frames                          */
+} ssk_planes;
+
+/* Window (WindowSpec) plus the SSIM constants (SsimConfig.c1/.c2,
+ * src/config.py:267-285).  taps = normalised 1-D Gaussian g/sum(g)
+ * (gaussian_kernel, src/stats.py:30-44, applied separably). */
+typedef struct ssk_window {
+  int32_t shape;    /* SSK_RECT or SSK_GAUSS                               */
+  int32_t k;        /* window size (gauss: odd, 3..31; rect: 1..4096)      */
+  int32_t stride;   /* >= 1                                                */
+  int32_t _pad;
+  double c1, c2;    /* (k1*L)^2, (k2*L)^2                                  */
+  float taps[32];   /* gauss only                                          */
+} ssk_window;
+
+/* ------------------------------------------------------------------------ */
+
+int ssk_abi_version(void);
+const char* ssk_strerror(int code);
+
+/* Workspace for ssk_ssim / ssk_msssim over this batch geometry. */
+size_t ssk_ssim_workspace_bytes(const ssk_planes* p, const ssk_window* win);
+size_t ssk_msssim_workspace_bytes(const ssk_planes* p, const ssk_window* win, int levels);
+
+/*
+ * Fused local statistics + SSIM terms + mean-pooling reduction for a batch.
+ * Replaces local_statistics (src/stats.py:205-261: _sliding_weighted_sums
+ * :155-164 for Gaussian windows, build_integral_set/_grid_window_sums
+ * :96-141 for rect windows), stats_from_sums (:185-202),
+ * term_maps_from_stats (src/ssim.py:31-46) and mssim (src/ssim.py:55-65).
+ *   d_sums  : [n][3] float64, per-frame (sum q, sum l, sum cs) over the grid
+ *             (only the components selected by `want` are meaningful).
+ *   d_maps  : optional; SSK_MAP_TERMS -> [n][3][gh][gw] (l, cs, q),
+ *             SSK_MAP_STATS -> [n][5][gh][gw] (mu1, mu2, var1, var2, cov);
+ *             float32 for Gaussian windows, float64 for rect windows.
+ * Rect windows on integer samples use exact integer window sums (the
+ * integral engine's int64 arithmetic, src/stats.py:101-103) and a float64
+ * epilogue in the reference's operation order, so their maps are
+ * bit-identical to the reference.
+ */
+int ssk_ssim(const ssk_planes* p, const ssk_window* win, int want,
+             double* d_sums, void* d_maps, void* d_workspace, size_t workspace_bytes,
+             void* stream);
+
+/*
+ * Exact integer window sums for a rect window on integer samples:
+ * d_out [n][5][gh][gw] int64 = the five grids
+ * _grid_window_sums(build_integral_set(ref, dist).table(t), k, s)
+ * for t in (sum1, sum2, sq1, sq2, prod) (src/stats.py:96-141), bit-exact.
+ */
+int ssk_box_window_sums(const ssk_planes* p, int k, int stride, int64_t* d_out,
+                        void* d_workspace, size_t workspace_bytes, void* stream);
+/* workspace: ssk_ssim_workspace_bytes(p, rect window k/stride) */
+
+/*
+ * Summed-area tables (src/stats.py:66-71, build_integral_set :96-116):
+ * d_out [n][5][h+1][w+1], int64 for integer samples (exact) or float64.
+ */
+int ssk_integral_tables(const ssk_planes* p, void* d_out, void* stream);
+
+/*
+ * 2x2 mean pyramid step (dyadic_downsample, src/multiscale.py:19-33).
+ * Integer inputs produce stored sums of 4 (dst scale_log2 = src + 2, exact);
+ * float inputs produce ((a00+a01)+a10)+a11)/4 in their own precision.
+ * dst: [n][h/2][w/2] with the given pitch, dtype dst_dtype.
+ */
+int ssk_downsample(const ssk_planes* src, void* d_dst_ref, void* d_dst_dist, int dst_dtype,
+                   int64_t dst_row_pitch, int64_t dst_frame_pitch, void* stream);
+
+/*
+ * Whole MS-SSIM pyramid for a batch (scale_scores, src/multiscale.py:36-59):
+ * d_level_means [n][levels] float64 = mean(cs) for levels < L-1 and
+ * mean(l*cs) at the coarsest level.  If d_ssim_sums is non-null, level 0
+ * also yields the plain-SSIM sums [n][3] (sum q, sum l, sum cs) of the same
+ * pass (scale 0 is shared).  The exponent-weighted combination
+ * (combine_scale_scores, :62-74) is done by the caller in float64.
+ */
+int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels,
+               double* d_level_means, double* d_ssim_sums,
+               void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* Number of kernels this library has launched since load (for bench.py). */
+uint64_t ssk_launch_count(void);
+
+/* Sustained FP32 FMA throughput probe (roofline denominator), TFLOP/s. */
+int ssk_probe_fp32_tflops(double seconds, double* tflops, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSIMK_H */

@@ -1,0 +1,231 @@
+"""CPU ORACLE — test infrastructure only, never part of the product path.
+
+A float64/int64 numpy restatement of the reference's SSIM hot path
+(ssimkit, /root/reference/pkg/src/ssimkit), written independently of the
+reference sources but replaying the same algorithms and the same arithmetic
+order, so that its outputs are bit-identical to the reference's:
+
+  gaussian_kernel ........ src/stats.py:30-44
+  sat / integral_set ..... src/stats.py:66-71, :96-116   (int64 for integer samples)
+  grid_window_sums ....... src/stats.py:130-141         (four-corner rule)
+  sliding_sums ........... src/stats.py:144-164         (direct k^2 loops)
+  moments_from_sums ...... src/stats.py:185-202
+  local_statistics ....... src/stats.py:205-261         (engine resolution :223-228)
+  term_maps .............. src/ssim.py:31-46
+  dyadic_downsample ...... src/multiscale.py:19-33
+  scale_scores / combine . src/multiscale.py:36-74
+  channel_scores ......... src/color.py:111-153         (cw / fixed models)
+  pool_temporal_am ....... src/pooling.py:254-255
+
+Parity pinning: tests/test_oracle_golden.py checks this module against
+golden vectors produced by the reference itself (tests/golden/make_golden.py,
+run in the build container where /root/reference is importable) and against
+the reference tests' known-answer values.
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg may
+import this module.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+STANDARD_EXPONENTS = (0.0448, 0.2856, 0.3001, 0.2363, 0.1333)
+
+
+def constants(bit_depth: int = 8, k1: float = 0.01, k2: float = 0.03) -> tuple[float, float]:
+    """C1 = (k1 L)^2, C2 = (k2 L)^2 with L = 2^bd - 1 (src/config.py:267-285)."""
+    peak = float((1 << bit_depth) - 1)
+    return (k1 * peak) ** 2, (k2 * peak) ** 2
+
+
+def default_gaussian_size(sigma: float) -> int:
+    return 2 * math.ceil(3.0 * sigma) + 1
+
+
+def gaussian_kernel(sigma: float, k: int | None = None) -> np.ndarray:
+    if k is None:
+        k = default_gaussian_size(sigma)
+    c = np.arange(k, dtype=np.float64) - (k - 1) / 2.0
+    g = np.exp(-(c * c) / (2.0 * sigma * sigma))
+    outer = np.outer(g, g)
+    return outer / outer.sum()
+
+
+# ---------------------------------------------------------------------------
+# window sums
+# ---------------------------------------------------------------------------
+
+def sat(values: np.ndarray) -> np.ndarray:
+    """(h+1) x (w+1) summed-area table with a zero first row and column."""
+    h, w = values.shape
+    table = np.zeros((h + 1, w + 1), dtype=values.dtype)
+    table[1:, 1:] = values.cumsum(axis=0).cumsum(axis=1)
+    return table
+
+
+def promote_pair(a: np.ndarray, b: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """int64 when both inputs are integer, else float64 (src/stats.py:101-106)."""
+    if a.dtype.kind in "ui" and b.dtype.kind in "ui":
+        return a.astype(np.int64), b.astype(np.int64)
+    return a.astype(np.float64), b.astype(np.float64)
+
+
+def integral_set(a: np.ndarray, b: np.ndarray) -> dict:
+    x, y = promote_pair(np.asarray(a), np.asarray(b))
+    return {"sum1": sat(x), "sum2": sat(y), "sq1": sat(x * x), "sq2": sat(y * y), "prod": sat(x * y)}
+
+
+def grid_window_sums(table: np.ndarray, k: int, stride: int) -> np.ndarray:
+    h, w = table.shape[0] - 1, table.shape[1] - 1
+    r_top, c_left = slice(0, h - k + 1, stride), slice(0, w - k + 1, stride)
+    r_bot, c_right = slice(k, h + 1, stride), slice(k, w + 1, stride)
+    return (table[r_bot, c_right] + table[r_top, c_left]) - (table[r_bot, c_left] + table[r_top, c_right])
+
+
+TABLES = ("sum1", "sum2", "sq1", "sq2", "prod")
+
+
+def box_window_sums(a: np.ndarray, b: np.ndarray, k: int, stride: int) -> np.ndarray:
+    """The five exact int64 grids the integral engine forms: [5, gh, gw]."""
+    iset = integral_set(a, b)
+    return np.stack([grid_window_sums(iset[t], k, stride) for t in TABLES])
+
+
+def sliding_sums(values: np.ndarray, weights: np.ndarray | None, k: int, stride: int) -> np.ndarray:
+    """Direct windowed (weighted) sums: accumulate the k^2 shifted, strided slices."""
+    h, w = values.shape
+    gh, gw = h - k + 1, w - k + 1
+    out = np.zeros(((gh - 1) // stride + 1, (gw - 1) // stride + 1), dtype=np.float64)
+    for m in range(k):
+        for n in range(k):
+            view = values[m:m + gh:stride, n:n + gw:stride]
+            out += view if weights is None else weights[m, n] * view
+    return out
+
+
+def moments_from_sums(s1, s2, q1, q2, p12, area: float):
+    mu1 = s1 / area
+    mu2 = s2 / area
+    var1 = np.maximum(q1 / area - mu1 * mu1, 0.0)
+    var2 = np.maximum(q2 / area - mu2 * mu2, 0.0)
+    cov = p12 / area - mu1 * mu2
+    return mu1, mu2, var1, var2, cov
+
+
+def local_statistics(a: np.ndarray, b: np.ndarray, shape: str, k: int, stride: int = 1,
+                     sigma: float | None = None, engine: str = "auto"):
+    """(mu1, mu2, var1, var2, cov) float64 grids."""
+    a, b = np.asarray(a), np.asarray(b)
+    h, w = a.shape
+    if k > h or k > w:
+        raise ValueError("window larger than image")
+    if engine == "auto":
+        engine = "integral" if shape == "rect" else "naive"
+    if engine == "integral" and shape != "rect":
+        raise ValueError("integral engine needs a rect window")
+    if engine == "integral":
+        iset = integral_set(a, b)
+        sums = [grid_window_sums(iset[t], k, stride).astype(np.float64) for t in TABLES]
+        return moments_from_sums(*sums, area=float(k * k))
+    fa = np.asarray(a, dtype=np.float64)
+    fb = np.asarray(b, dtype=np.float64)
+    weights = None if shape == "rect" else gaussian_kernel(sigma, k)
+    sums = [sliding_sums(v, weights, k, stride) for v in (fa, fb, fa * fa, fb * fb, fa * fb)]
+    return moments_from_sums(*sums, area=float(k * k) if shape == "rect" else 1.0)
+
+
+def term_maps(mu1, mu2, var1, var2, cov, c1: float, c2: float):
+    """(l, cs, q) float64 maps."""
+    l_map = (2.0 * mu1 * mu2 + c1) / (mu1 * mu1 + mu2 * mu2 + c1)
+    cs_map = (2.0 * cov + c2) / (var1 + var2 + c2)
+    return l_map, cs_map, l_map * cs_map
+
+
+def ssim_maps(a, b, shape: str = "rect", k: int = 11, stride: int = 1, sigma: float | None = None,
+              bit_depth: int = 8, k1: float = 0.01, k2: float = 0.03, engine: str = "auto"):
+    c1, c2 = constants(bit_depth, k1, k2)
+    return term_maps(*local_statistics(a, b, shape, k, stride, sigma, engine), c1, c2)
+
+
+def ssim_score(a, b, **window) -> float:
+    return float(ssim_maps(a, b, **window)[2].mean())
+
+
+def ssim_terms(a, b, **window) -> tuple[float, float, float]:
+    """(mean q, mean l, mean cs) — the pipeline's (score/am, l_mean, cs_mean) record."""
+    l_map, cs_map, q = ssim_maps(a, b, **window)
+    return float(q.mean()), float(l_map.mean()), float(cs_map.mean())
+
+
+# ---------------------------------------------------------------------------
+# multiscale
+# ---------------------------------------------------------------------------
+
+def dyadic_downsample(values: np.ndarray) -> np.ndarray:
+    arr = np.asarray(values, dtype=np.float64)
+    h2, w2 = arr.shape[0] // 2, arr.shape[1] // 2
+    arr = arr[: 2 * h2, : 2 * w2]
+    return (arr[0::2, 0::2] + arr[0::2, 1::2] + arr[1::2, 0::2] + arr[1::2, 1::2]) / 4.0
+
+
+def scale_scores(a, b, levels: int, **window) -> list[float]:
+    k = window.get("k", 11)
+    h, w = np.asarray(a).shape
+    if min(h, w) // (1 << (levels - 1)) < k:
+        raise ValueError("too many levels")
+    cur_a, cur_b = a, b
+    out = []
+    for level in range(levels):
+        if level > 0:
+            cur_a, cur_b = dyadic_downsample(cur_a), dyadic_downsample(cur_b)
+        _, cs_map, q = ssim_maps(cur_a, cur_b, **window)
+        out.append(float((q if level == levels - 1 else cs_map).mean()))
+    return out
+
+
+def effective_exponents(aggregation: str, exponents) -> tuple:
+    if aggregation in ("sum", "fast4"):
+        total = sum(exponents)
+        return tuple(e / total for e in exponents)
+    return tuple(exponents)
+
+
+def combine_scale_scores(scores, aggregation: str = "product", exponents=STANDARD_EXPONENTS) -> float:
+    exps = effective_exponents(aggregation, exponents)
+    if aggregation == "sum":
+        return float(sum(e * s for e, s in zip(exps, scores)))
+    out = 1.0
+    for e, s in zip(exps, scores):
+        out *= max(s, 0.0) ** e
+    return float(out)
+
+
+def msssim(a, b, levels: int = 5, aggregation: str = "product", exponents=None, **window) -> float:
+    if exponents is None:
+        exponents = STANDARD_EXPONENTS[:levels]
+    return combine_scale_scores(scale_scores(a, b, levels, **window), aggregation, exponents)
+
+
+# ---------------------------------------------------------------------------
+# color + temporal
+# ---------------------------------------------------------------------------
+
+def channel_scores(ref_planes, dist_planes, **window) -> tuple[float, float, float]:
+    """Per-channel mean SSIM, each plane at its own resolution (4:2:0 chroma stays 4:2:0)."""
+    return tuple(ssim_score(a, b, **window) for a, b in zip(ref_planes, dist_planes))
+
+
+def fixed_weight(scores, weights) -> float:
+    return float(sum(w * s for w, s in zip(weights, scores)))
+
+
+def channelwise(scores, alpha: float, beta: float) -> float:
+    fy, fcb, fcr = scores
+    return (fy + alpha * fcb + beta * fcr) / (1.0 + alpha + beta)
+
+
+def pool_temporal_am(scores) -> float:
+    return float(np.asarray(scores, dtype=np.float64).reshape(-1).mean())

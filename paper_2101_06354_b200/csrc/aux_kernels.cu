@@ -1,0 +1,234 @@
+// Auxiliary kernels: deterministic partial folding, the 2x2 pyramid step,
+// summed-area tables for the IntegralSet API, and the FP32 peak probe.
+#include <type_traits>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ssk {
+
+// ---------------------------------------------------------------------------
+// Fold per-CTA partials [n][nparts][ncomp] into out[f*out_stride + out_offset + c]
+// = mul * sum_p partials[f][p][comp_offset + c]; one warp per frame, fixed
+// order -> bit-reproducible run to run (the reference's ordered frame results,
+// tests/test_cli.py:124-130, rely on determinism).
+// ---------------------------------------------------------------------------
+__global__ void reduce_partials_kernel(const double* __restrict__ partials, int nparts, int n,
+                                       int ncomp, double mul, double* __restrict__ out,
+                                       int out_stride, int out_offset, int comp_offset) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const double* p = partials + (long long)warp * nparts * 3;
+  for (int c = 0; c < ncomp; ++c) {
+    double s = 0.0;
+    for (int i = lane; i < nparts; i += 32) s += p[(long long)i * 3 + comp_offset + c];
+    s = warp_sum(s);
+    if (lane == 0) out[(long long)warp * out_stride + out_offset + c] = s * mul;
+  }
+}
+
+int launch_reduce_partials(const double* partials, int nparts, int n, int ncomp, double mul,
+                           double* out, int out_stride, int out_offset, int comp_offset,
+                           cudaStream_t st) {
+  const int threads = 256;
+  const int blocks = (n * 32 + threads - 1) / threads;
+  reduce_partials_kernel<<<blocks, threads, 0, st>>>(partials, nparts, n, ncomp, mul, out,
+                                                     out_stride, out_offset, comp_offset);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+}
+
+// ---------------------------------------------------------------------------
+// dyadic_downsample (src/multiscale.py:19-33): 2x2 block over the even-trimmed
+// plane.  Integer planes keep the exact sum of the four samples (the caller
+// tracks the 4^-s scale); float planes compute ((a00+a01)+a10)+a11 then /4
+// exactly like the reference's numpy expression.
+// ---------------------------------------------------------------------------
+template <typename TS, typename TD>
+__global__ void downsample_kernel(const unsigned char* __restrict__ src_r,
+                                  const unsigned char* __restrict__ src_d, long long src_rp,
+                                  long long src_fp, int h2, int w2, unsigned char* __restrict__ dst_r,
+                                  unsigned char* __restrict__ dst_d, long long dst_rp,
+                                  long long dst_fp) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  const int f = blockIdx.z >> 1;
+  const int img = blockIdx.z & 1;
+  if (x >= w2) return;
+  const TS* s = reinterpret_cast<const TS*>((img ? src_d : src_r)) + f * src_fp;
+  TD* d = reinterpret_cast<TD*>((img ? dst_d : dst_r)) + f * dst_fp;
+  const TS* r0 = s + (long long)(2 * y) * src_rp + 2 * x;
+  const TS* r1 = r0 + src_rp;
+  if constexpr (std::is_floating_point<TS>::value) {
+    d[(long long)y * dst_rp + x] = (TD)((((r0[0] + r0[1]) + r1[0]) + r1[1]) / (TS)4);
+  } else {
+    d[(long long)y * dst_rp + x] = (TD)((uint32_t)r0[0] + r0[1] + r1[0] + r1[1]);
+  }
+}
+
+template <typename TS, typename TD>
+static void ds_launch(const unsigned char* sr, const unsigned char* sd, long long srp, long long sfp,
+                      int n, int h2, int w2, unsigned char* dr, unsigned char* dd, long long drp,
+                      long long dfp, cudaStream_t st) {
+  dim3 block(128);
+  dim3 grid((w2 + 127) / 128, h2, 2 * n);
+  downsample_kernel<TS, TD><<<grid, block, 0, st>>>(sr, sd, srp, sfp, h2, w2, dr, dd, drp, dfp);
+}
+
+int launch_downsample(const unsigned char* src_r, const unsigned char* src_d, int src_dtype,
+                      long long src_rp, long long src_fp, int n, int h, int w,
+                      unsigned char* dst_r, unsigned char* dst_d, int dst_dtype, long long dst_rp,
+                      long long dst_fp, cudaStream_t st) {
+  const int h2 = h / 2, w2 = w / 2;
+  if (h2 < 1 || w2 < 1) return SSK_E_TOO_SMALL;
+  if (2 * n > 65535 || h2 > 65535) return SSK_E_ARG;
+#define DS(TS, TD) ds_launch<TS, TD>(src_r, src_d, src_rp, src_fp, n, h2, w2, dst_r, dst_d, dst_rp, dst_fp, st)
+  if (src_dtype == SSK_U8 && dst_dtype == SSK_U16) DS(uint8_t, uint16_t);
+  else if (src_dtype == SSK_U8 && dst_dtype == SSK_U32) DS(uint8_t, uint32_t);
+  else if (src_dtype == SSK_U16 && dst_dtype == SSK_U16) DS(uint16_t, uint16_t);
+  else if (src_dtype == SSK_U16 && dst_dtype == SSK_U32) DS(uint16_t, uint32_t);
+  else if (src_dtype == SSK_U32 && dst_dtype == SSK_U32) DS(uint32_t, uint32_t);
+  else if (src_dtype == SSK_F32 && dst_dtype == SSK_F32) DS(float, float);
+  else if (src_dtype == SSK_F64 && dst_dtype == SSK_F64) DS(double, double);
+  else return SSK_E_ARG;
+#undef DS
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+}
+
+// ---------------------------------------------------------------------------
+// Summed-area tables (src/stats.py:66-71): out[f][t][h+1][w+1] with a zero
+// first row/column; t = (x, y, x^2, y^2, xy).  The reference takes
+// cumsum(axis=0) then cumsum(axis=1), sequentially; the same order is kept
+// (column pass then row pass), so float64 tables match bit for bit and
+// integer tables are exact int64.
+// ---------------------------------------------------------------------------
+template <typename TS, typename TA>
+__global__ void sat_column_kernel(const unsigned char* __restrict__ ref,
+                                  const unsigned char* __restrict__ dist, long long rp, long long fp,
+                                  int h, int w, TA* __restrict__ out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int f = blockIdx.y;
+  if (x > w) return;
+  const long long plane = (long long)(h + 1) * (w + 1);
+  TA* o = out + (long long)f * 5 * plane;
+  for (int t = 0; t < 5; ++t) o[t * plane + x] = 0;  // zero first row
+  if (x == 0) {
+    for (int y = 1; y <= h; ++y)
+      for (int t = 0; t < 5; ++t) o[t * plane + (long long)y * (w + 1)] = 0;
+    return;
+  }
+  const TS* a = reinterpret_cast<const TS*>(ref) + f * fp + (x - 1);
+  const TS* b = reinterpret_cast<const TS*>(dist) + f * fp + (x - 1);
+  TA acc[5] = {0, 0, 0, 0, 0};
+  for (int y = 0; y < h; ++y) {
+    const TA va = (TA)a[(long long)y * rp], vb = (TA)b[(long long)y * rp];
+    acc[0] += va;
+    acc[1] += vb;
+    acc[2] += va * va;
+    acc[3] += vb * vb;
+    acc[4] += va * vb;
+    for (int t = 0; t < 5; ++t) o[t * plane + (long long)(y + 1) * (w + 1) + x] = acc[t];
+  }
+}
+
+template <typename TA>
+__global__ void sat_row_kernel(int h, int w, TA* __restrict__ out) {
+  const int y = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  const int t = blockIdx.y;
+  const int f = blockIdx.z;
+  if (y > h) return;
+  const long long plane = (long long)(h + 1) * (w + 1);
+  TA* row = out + ((long long)f * 5 + t) * plane + (long long)y * (w + 1);
+  TA acc = 0;
+  for (int x = 1; x <= w; ++x) {
+    acc += row[x];
+    row[x] = acc;
+  }
+}
+
+int launch_integral(const unsigned char* ref, const unsigned char* dist, int dtype, long long rp,
+                    long long fp, int n, int h, int w, void* out, cudaStream_t st) {
+  dim3 gc((w + 1 + 127) / 128, n), gr((h + 127) / 128, 5, n);
+  switch (dtype) {
+    case SSK_U8:
+      sat_column_kernel<uint8_t, long long><<<gc, 128, 0, st>>>(ref, dist, rp, fp, h, w, (long long*)out);
+      sat_row_kernel<long long><<<gr, 128, 0, st>>>(h, w, (long long*)out);
+      break;
+    case SSK_U16:
+      sat_column_kernel<uint16_t, long long><<<gc, 128, 0, st>>>(ref, dist, rp, fp, h, w, (long long*)out);
+      sat_row_kernel<long long><<<gr, 128, 0, st>>>(h, w, (long long*)out);
+      break;
+    case SSK_U32:
+      sat_column_kernel<uint32_t, long long><<<gc, 128, 0, st>>>(ref, dist, rp, fp, h, w, (long long*)out);
+      sat_row_kernel<long long><<<gr, 128, 0, st>>>(h, w, (long long*)out);
+      break;
+    case SSK_F32:
+      sat_column_kernel<float, double><<<gc, 128, 0, st>>>(ref, dist, rp, fp, h, w, (double*)out);
+      sat_row_kernel<double><<<gr, 128, 0, st>>>(h, w, (double*)out);
+      break;
+    case SSK_F64:
+      sat_column_kernel<double, double><<<gc, 128, 0, st>>>(ref, dist, rp, fp, h, w, (double*)out);
+      sat_row_kernel<double><<<gr, 128, 0, st>>>(h, w, (double*)out);
+      break;
+    default:
+      return SSK_E_ARG;
+  }
+  note_launch(2);
+  return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+}
+
+// ---------------------------------------------------------------------------
+// FP32 FMA probe: 16 independent register-form FFMA chains per thread.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) fp32_probe_kernel(float* out, int iters, float b, float c) {
+  float acc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i] = threadIdx.x * 1e-6f + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] = fmaf(acc[i], b, c);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += acc[i];
+  if (s == 1234.5f) out[0] = s;
+}
+
+int probe_fp32(double seconds, double* tflops, cudaStream_t st) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  float* d = nullptr;
+  if (cudaMalloc(&d, 4) != cudaSuccess) return SSK_E_CUDA;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 8, threads = 256, iters = 20000;
+  const double flops_per_launch = 2.0 * blocks * threads * (double)iters * 8 * 16;
+  fp32_probe_kernel<<<blocks, threads, 0, st>>>(d, iters, 1.0001f, 0.5f);  // warm-up
+  note_launch();
+  cudaEventRecord(e0, st);
+  int launches = 0;
+  float ms = 0.f;
+  do {
+    fp32_probe_kernel<<<blocks, threads, 0, st>>>(d, iters, 1.0001f, 0.5f);
+    note_launch();
+    ++launches;
+    if (launches % 8 == 0) {
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+    }
+  } while (ms < seconds * 1e3);
+  *tflops = flops_per_launch * launches / (ms * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+}
+
+}  // namespace ssk

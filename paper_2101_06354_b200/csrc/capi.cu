@@ -1,0 +1,402 @@
+// C ABI entry points (include/ssimk.h): argument validation, launch planning,
+// workspace carving and the MS-SSIM level loop.  Host-side C++; no allocation
+// inside the calls (all scratch comes from the caller's workspace).
+#include <atomic>
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ssk {
+
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch(int count) { g_launches.fetch_add((unsigned long long)count); }
+int probe_fp32(double seconds, double* tflops, cudaStream_t st);
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
+
+struct Plan {
+  bool gauss = false;
+  bool box_int = false;
+  bool wide = false;
+  dim3 grid, block;
+  int gh = 0, gw = 0;
+  size_t nparts_per_frame = 0;
+  GaussArgs ga{};
+  BoxArgs ba{};
+};
+
+int check_planes(const ssk_planes* p) {
+  if (!p || !p->ref || !p->dist) return SSK_E_ARG;
+  const int es = esize_of(p->dtype);
+  if (es == 0) return SSK_E_ARG;
+  if (p->n < 1 || p->h < 1 || p->w < 1 || p->n > 65535) return SSK_E_ARG;
+  if (p->row_pitch < p->w || p->frame_pitch < p->row_pitch * (int64_t)p->h) return SSK_E_ARG;
+  if (p->bit_depth < 8 || p->bit_depth > 16 || p->scale_log2 < 0 || p->scale_log2 > 40)
+    return SSK_E_ARG;
+  if ((reinterpret_cast<uintptr_t>(p->ref) & 15) || (reinterpret_cast<uintptr_t>(p->dist) & 15) ||
+      ((p->row_pitch * es) & 15) || ((p->frame_pitch * es) & 15))
+    return SSK_E_ALIGN;
+  return SSK_OK;
+}
+
+int check_window(const ssk_planes* p, const ssk_window* win) {
+  if (!win || win->k < 1 || win->stride < 1) return SSK_E_ARG;
+  if (win->shape == SSK_GAUSS) {
+    if (win->k < 3 || (win->k % 2) == 0 || win->k > 31) return SSK_E_SHAPE;
+    if (p->dtype == SSK_F64) return SSK_E_ARG;
+  } else if (win->shape != SSK_RECT) {
+    return SSK_E_ARG;
+  }
+  if (win->k > p->h || win->k > p->w) return SSK_E_WINDOW;
+  return SSK_OK;
+}
+
+int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
+  int rc = check_planes(p);
+  if (rc) return rc;
+  rc = check_window(p, win);
+  if (rc) return rc;
+  const int k = win->k, s = win->stride;
+  const int es = esize_of(p->dtype);
+  pl.gh = grid_extent(p->h, k, s);
+  pl.gw = grid_extent(p->w, k, s);
+  const double L = std::ldexp(1.0, p->bit_depth) - 1.0;
+  const double stored_max = L * std::ldexp(1.0, p->scale_log2);
+
+  if (win->shape == SSK_GAUSS) {
+    pl.gauss = true;
+    GaussArgs& a = pl.ga;
+    a.ref = static_cast<const unsigned char*>(p->ref);
+    a.dist = static_cast<const unsigned char*>(p->dist);
+    a.row_pitch_b = p->row_pitch * es;
+    a.frame_pitch_b = p->frame_pitch * es;
+    a.dtype = p->dtype;
+    a.esize = es;
+    a.n = p->n;
+    a.h = p->h;
+    a.w = p->w;
+    a.ho = p->h - k + 1;
+    a.wo = p->w - k + 1;
+    a.gh = pl.gh;
+    a.gw = pl.gw;
+    a.stride = s;
+    const int nstrips = (a.wo + GS_TW - 1) / GS_TW;
+    const long long target = 2368;  // >= 4 waves of 148 SMs x 4 resident CTAs
+    int nseg = (a.ho + 127) / 128;
+    const long long want_seg = (target + (long long)nstrips * p->n - 1) / ((long long)nstrips * p->n);
+    const int max_seg = (a.ho + 31) / 32;
+    if (want_seg > nseg) nseg = (int)(want_seg < max_seg ? want_seg : max_seg);
+    if (nseg < 1) nseg = 1;
+    a.seg_rows = (a.ho + nseg - 1) / nseg;
+    nseg = (a.ho + a.seg_rows - 1) / a.seg_rows;
+    a.in_pitch = gauss_in_pitch(k, es);
+    const float shift = (float)std::ldexp(1.0, p->bit_depth - 1);
+    const double scale = std::ldexp(1.0, -p->scale_log2);
+    a.conv_scale = (p->dtype == SSK_F32) ? 1.0f : (float)scale;
+    if (p->dtype == SSK_U8 || p->dtype == SSK_U16)
+      a.conv_bias = (float)(-(8388608.0 * scale + shift));
+    else
+      a.conv_bias = -shift;
+    a.shift = shift;
+    a.c1 = (float)win->c1;
+    a.c2 = (float)win->c2;
+    a.want = want;
+    std::memcpy(a.taps, win->taps, sizeof(a.taps));
+    pl.grid = dim3(nstrips, nseg, p->n);
+    pl.nparts_per_frame = (size_t)nstrips * nseg;
+    a.map_plane = (long long)pl.gh * pl.gw;
+    a.map_frame = a.map_plane * ((want & SSK_MAP_STATS) ? 5 : 3);
+    return SSK_OK;
+  }
+
+  BoxArgs& a = pl.ba;
+  a.ref = static_cast<const unsigned char*>(p->ref);
+  a.dist = static_cast<const unsigned char*>(p->dist);
+  a.row_pitch_b = p->row_pitch * es;
+  a.frame_pitch_b = p->frame_pitch * es;
+  a.dtype = p->dtype;
+  a.esize = es;
+  a.n = p->n;
+  a.h = p->h;
+  a.w = p->w;
+  a.k = k;
+  a.s = s;
+  a.gh = pl.gh;
+  a.gw = pl.gw;
+  a.sscale1 = std::ldexp(1.0, -p->scale_log2);
+  a.sscale2 = std::ldexp(1.0, -2 * p->scale_log2);
+  a.area = (double)k * (double)k;
+  int ex = 0;
+  const double fr = std::frexp(a.area, &ex);
+  a.area_pow2 = (fr == 0.5) ? 1 : 0;
+  a.inv_area = 1.0 / a.area;
+  a.c1 = win->c1;
+  a.c2 = win->c2;
+  a.want = want;
+  a.map_plane = (long long)pl.gh * pl.gw;
+  a.map_frame = a.map_plane * ((want & SSK_MAP_STATS) ? 5 : 3);
+  a.wsums = nullptr;
+  const bool integer = p->dtype == SSK_U8 || p->dtype == SSK_U16 || p->dtype == SSK_U32;
+  if (integer && k <= BX_THREADS) {
+    pl.box_int = true;
+    pl.wide = (double)k * k * stored_max * stored_max >= 4294967296.0;
+    a.na = (BX_THREADS - k) / s + 1;
+    const int nstrips = (pl.gw + a.na - 1) / a.na;
+    int vr = 32 / s;
+    vr = vr < 1 ? 1 : (vr > 8 ? 8 : vr);
+    a.ch = vr * s;
+    a.in_pitch = BX_THREADS * es + 16;
+    a.nslot = (k + s - 1) / s + 1;
+    int seg_anchors = (256 + s - 1) / s;
+    if (seg_anchors < 1) seg_anchors = 1;
+    // enough CTAs for small batches: split rows further (down to ~32 input rows)
+    const long long target = 2368;
+    long long nseg = (pl.gh + seg_anchors - 1) / seg_anchors;
+    const long long have = (long long)nstrips * p->n * nseg;
+    if (have < target) {
+      const int min_anchors = (32 + s - 1) / s;
+      long long want_seg = (target + (long long)nstrips * p->n - 1) / ((long long)nstrips * p->n);
+      int sa = (int)((pl.gh + want_seg - 1) / want_seg);
+      seg_anchors = sa < min_anchors ? min_anchors : sa;
+    }
+    a.seg_anchors = seg_anchors;
+    nseg = (pl.gh + seg_anchors - 1) / seg_anchors;
+    if (nseg > 65535) return SSK_E_ARG;
+    pl.grid = dim3(nstrips, (unsigned)nseg, p->n);
+    pl.nparts_per_frame = (size_t)nstrips * nseg;
+    if (box_smem_bytes(a, pl.wide) > 227 * 1024) {
+      pl.box_int = false;  // extreme strides: fall through to the direct kernel
+    } else {
+      return SSK_OK;
+    }
+  }
+  pl.block = dim3(32, 4);
+  pl.grid = dim3((pl.gw + 31) / 32, (pl.gh + 3) / 4, p->n);
+  if (pl.grid.y > 65535) return SSK_E_ARG;
+  pl.nparts_per_frame = (size_t)pl.grid.x * pl.grid.y;
+  return SSK_OK;
+}
+
+size_t partial_bytes(const Plan& pl, int n) { return align_up(pl.nparts_per_frame * n * 3 * sizeof(double)); }
+
+int run_plan(Plan& pl, double* partials, void* maps, long long* wsums, cudaStream_t st) {
+  if (pl.gauss) {
+    pl.ga.partials = partials;
+    pl.ga.maps = maps;
+    return launch_gauss(pl.ga, pl.grid, pl.ga.h - pl.ga.ho + 1, st);
+  }
+  pl.ba.partials = partials;
+  pl.ba.maps = static_cast<double*>(maps);
+  pl.ba.wsums = wsums;
+  if (pl.box_int) return launch_box_int(pl.ba, pl.grid, pl.wide, st);
+  return launch_box_float(pl.ba, pl.grid, pl.block, st);
+}
+
+// ---- MS-SSIM pyramid layout ----
+struct Level {
+  ssk_planes planes;
+  size_t offset_r = 0, offset_d = 0;  // workspace offsets (level >= 1)
+};
+
+int level_dtype(const ssk_planes* p, int level) {
+  if (p->dtype == SSK_F32) return SSK_F32;
+  if (p->dtype == SSK_F64) return SSK_F64;
+  const double mx = (std::ldexp(1.0, p->bit_depth) - 1.0) * std::ldexp(1.0, p->scale_log2 + 2 * level);
+  return mx <= 65535.0 ? SSK_U16 : SSK_U32;
+}
+
+int plan_pyramid(const ssk_planes* p, const ssk_window* win, int levels, Level* lv, size_t* pyr_bytes) {
+  size_t off = 0;
+  lv[0].planes = *p;
+  for (int l = 1; l < levels; ++l) {
+    const ssk_planes& prev = lv[l - 1].planes;
+    ssk_planes q = prev;
+    q.h = prev.h / 2;
+    q.w = prev.w / 2;
+    if (q.h < 1 || q.w < 1) return SSK_E_TOO_SMALL;
+    q.dtype = level_dtype(p, l);
+    if (q.dtype == SSK_U16 || q.dtype == SSK_U32) q.scale_log2 = p->scale_log2 + 2 * l;
+    const int es = esize_of(q.dtype);
+    q.row_pitch = (int64_t)(align_up((size_t)q.w * es, 16) / es);
+    q.frame_pitch = q.row_pitch * q.h;
+    const size_t bytes = align_up((size_t)q.frame_pitch * es * q.n);
+    lv[l].offset_r = off;
+    off += bytes;
+    lv[l].offset_d = off;
+    off += bytes;
+    lv[l].planes = q;
+  }
+  (void)win;
+  *pyr_bytes = off;
+  return SSK_OK;
+}
+
+}  // namespace
+}  // namespace ssk
+
+using namespace ssk;
+
+extern "C" {
+
+int ssk_abi_version(void) { return SSK_ABI_VERSION; }
+
+const char* ssk_strerror(int code) {
+  switch (code) {
+    case SSK_OK: return "ok";
+    case SSK_E_ARG: return "invalid argument";
+    case SSK_E_WINDOW: return "window larger than the image";
+    case SSK_E_SHAPE: return "unsupported window shape/size for this engine";
+    case SSK_E_WORKSPACE: return "workspace too small";
+    case SSK_E_ALIGN: return "planes must be 16-byte aligned with 16-byte row/frame pitches";
+    case SSK_E_CUDA: return "CUDA error";
+    case SSK_E_LEVELS: return "too many scales for the image size";
+    case SSK_E_TOO_SMALL: return "plane too small to downsample";
+    default: return "unknown error";
+  }
+}
+
+size_t ssk_ssim_workspace_bytes(const ssk_planes* p, const ssk_window* win) {
+  Plan pl;
+  if (plan_ssim(p, win, SSK_WANT_Q | SSK_WANT_L | SSK_WANT_CS, pl)) return 0;
+  return partial_bytes(pl, p->n);
+}
+
+int ssk_ssim(const ssk_planes* p, const ssk_window* win, int want, double* d_sums, void* d_maps,
+             void* d_workspace, size_t workspace_bytes, void* stream) {
+  Plan pl;
+  const int rc = plan_ssim(p, win, want, pl);
+  if (rc) return rc;
+  if (!d_sums) return SSK_E_ARG;
+  if ((want & (SSK_MAP_TERMS | SSK_MAP_STATS)) && !d_maps) return SSK_E_ARG;
+  const size_t need = partial_bytes(pl, p->n);
+  if (!d_workspace || workspace_bytes < need) return SSK_E_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* partials = static_cast<double*>(d_workspace);
+  int e = run_plan(pl, partials, d_maps, nullptr, st);
+  if (e) return e;
+  return launch_reduce_partials(partials, (int)pl.nparts_per_frame, p->n, 3, 1.0, d_sums, 3, 0, 0, st);
+}
+
+int ssk_box_window_sums(const ssk_planes* p, int k, int stride, int64_t* d_out, void* d_workspace,
+                        size_t workspace_bytes, void* stream) {
+  if (!d_out || !p) return SSK_E_ARG;
+  if (p->dtype == SSK_F32 || p->dtype == SSK_F64) return SSK_E_ARG;
+  ssk_window win{};
+  win.shape = SSK_RECT;
+  win.k = k;
+  win.stride = stride;
+  win.c1 = 1.0;
+  win.c2 = 1.0;
+  Plan pl;
+  const int rc = plan_ssim(p, &win, SSK_WANT_Q, pl);
+  if (rc) return rc;
+  if (!d_workspace || workspace_bytes < partial_bytes(pl, p->n)) return SSK_E_WORKSPACE;
+  return run_plan(pl, static_cast<double*>(d_workspace), nullptr, reinterpret_cast<long long*>(d_out),
+                  static_cast<cudaStream_t>(stream));
+}
+
+int ssk_integral_tables(const ssk_planes* p, void* d_out, void* stream) {
+  const int rc = check_planes(p);
+  if (rc) return rc;
+  if (!d_out) return SSK_E_ARG;
+  return launch_integral(static_cast<const unsigned char*>(p->ref),
+                         static_cast<const unsigned char*>(p->dist), p->dtype, p->row_pitch,
+                         p->frame_pitch, p->n, p->h, p->w, d_out, static_cast<cudaStream_t>(stream));
+}
+
+int ssk_downsample(const ssk_planes* src, void* d_dst_ref, void* d_dst_dist, int dst_dtype,
+                   int64_t dst_row_pitch, int64_t dst_frame_pitch, void* stream) {
+  if (!src || !src->ref || !src->dist || !d_dst_ref || !d_dst_dist) return SSK_E_ARG;
+  if (esize_of(src->dtype) == 0 || esize_of(dst_dtype) == 0 || src->n < 1) return SSK_E_ARG;
+  if (src->h < 2 || src->w < 2) return SSK_E_TOO_SMALL;
+  return launch_downsample(static_cast<const unsigned char*>(src->ref),
+                           static_cast<const unsigned char*>(src->dist), src->dtype, src->row_pitch,
+                           src->frame_pitch, src->n, src->h, src->w,
+                           static_cast<unsigned char*>(d_dst_ref), static_cast<unsigned char*>(d_dst_dist),
+                           dst_dtype, dst_row_pitch, dst_frame_pitch, static_cast<cudaStream_t>(stream));
+}
+
+size_t ssk_msssim_workspace_bytes(const ssk_planes* p, const ssk_window* win, int levels) {
+  if (!p || levels < 1 || levels > 16) return 0;
+  Level lv[16];
+  size_t pyr = 0;
+  if (plan_pyramid(p, win, levels, lv, &pyr)) return 0;
+  size_t parts = 0;
+  for (int l = 0; l < levels; ++l) {
+    ssk_planes q = lv[l].planes;
+    if (l > 0) q.ref = q.dist = reinterpret_cast<const void*>(kAlign);  // lives in the workspace
+    Plan pl;
+    if (plan_ssim(&q, win, SSK_WANT_Q | SSK_WANT_L | SSK_WANT_CS, pl)) return 0;
+    parts += partial_bytes(pl, p->n);
+  }
+  return pyr + parts;
+}
+
+int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, double* d_level_means,
+               double* d_ssim_sums, void* d_workspace, size_t workspace_bytes, void* stream) {
+  int rc = check_planes(p);
+  if (rc) return rc;
+  if (!win || !d_level_means || levels < 1 || levels > 16) return SSK_E_ARG;
+  if ((std::min(p->h, p->w) >> (levels - 1)) < win->k) return SSK_E_LEVELS;
+  const size_t need = ssk_msssim_workspace_bytes(p, win, levels);
+  if (need == 0) return SSK_E_ARG;
+  if (!d_workspace || workspace_bytes < need) return SSK_E_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned char* ws = static_cast<unsigned char*>(d_workspace);
+  Level lv[16];
+  size_t pyr = 0;
+  rc = plan_pyramid(p, win, levels, lv, &pyr);
+  if (rc) return rc;
+  for (int l = 1; l < levels; ++l) {
+    lv[l].planes.ref = ws + lv[l].offset_r;
+    lv[l].planes.dist = ws + lv[l].offset_d;
+  }
+  size_t part_off = pyr;
+  for (int l = 0; l < levels; ++l) {
+    if (l > 0) {
+      const ssk_planes& a = lv[l - 1].planes;
+      const ssk_planes& b = lv[l].planes;
+      rc = launch_downsample(static_cast<const unsigned char*>(a.ref),
+                             static_cast<const unsigned char*>(a.dist), a.dtype, a.row_pitch,
+                             a.frame_pitch, a.n, a.h, a.w,
+                             const_cast<unsigned char*>(static_cast<const unsigned char*>(b.ref)),
+                             const_cast<unsigned char*>(static_cast<const unsigned char*>(b.dist)),
+                             b.dtype, b.row_pitch, b.frame_pitch, st);
+      if (rc) return rc;
+    }
+    const bool last = l == levels - 1;
+    int want = last ? SSK_WANT_Q : SSK_WANT_CS;
+    if (l == 0 && d_ssim_sums) want |= SSK_WANT_Q | SSK_WANT_L | SSK_WANT_CS;
+    Plan pl;
+    rc = plan_ssim(&lv[l].planes, win, want, pl);
+    if (rc) return rc;
+    double* partials = reinterpret_cast<double*>(ws + part_off);
+    part_off += partial_bytes(pl, p->n);
+    rc = run_plan(pl, partials, nullptr, nullptr, st);
+    if (rc) return rc;
+    const double inv_count = 1.0 / ((double)pl.gh * (double)pl.gw);
+    rc = launch_reduce_partials(partials, (int)pl.nparts_per_frame, p->n, 1, inv_count,
+                                d_level_means, levels, l, last ? 0 : 2, st);
+    if (rc) return rc;
+    if (l == 0 && d_ssim_sums) {
+      rc = launch_reduce_partials(partials, (int)pl.nparts_per_frame, p->n, 3, 1.0, d_ssim_sums, 3,
+                                  0, 0, st);
+      if (rc) return rc;
+    }
+  }
+  return SSK_OK;
+}
+
+uint64_t ssk_launch_count(void) { return g_launches.load(); }
+
+int ssk_probe_fp32_tflops(double seconds, double* tflops, void* stream) {
+  if (!tflops || seconds <= 0) return SSK_E_ARG;
+  return probe_fp32(seconds, tflops, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

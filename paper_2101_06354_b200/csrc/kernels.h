@@ -1,0 +1,79 @@
+// Internal kernel argument blocks and launchers (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ssk {
+
+// ---------------- K1: Gaussian window ----------------
+constexpr int GS_THREADS = 128;  // one output column per thread in the V pass
+constexpr int GS_TW = 128;       // output columns per strip
+constexpr int GS_G = 8;          // input rows per chunk
+constexpr int GS_HP = 132;       // ring row pitch in floats (== 4 mod 32: conflict-free float4 rows)
+
+struct GaussArgs {
+  const unsigned char* ref;
+  const unsigned char* dist;
+  long long row_pitch_b, frame_pitch_b;  // bytes
+  int dtype, esize;
+  int n, h, w;
+  int ho, wo;                 // dense output extents (h-k+1, w-k+1)
+  int gh, gw, stride;         // anchor grid
+  int seg_rows;               // output rows per segment (gridDim.y segments)
+  int in_pitch;               // staging row pitch, bytes
+  float conv_scale, conv_bias;  // shifted sample = fma(raw_or_biased, scale, bias)
+  float shift;                // added back to the means
+  float c1, c2;
+  int want;
+  float taps[32];
+  double* partials;           // [n][gridDim.y][gridDim.x][3]
+  void* maps;                 // float32 [n][planes][gh][gw]
+  long long map_plane, map_frame;
+};
+
+int gauss_in_pitch(int k, int esize);
+size_t gauss_smem_bytes(int k, int in_pitch);
+int launch_gauss(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
+
+// ---------------- K2: rect window ----------------
+constexpr int BX_THREADS = 128;  // one input column per thread in the V pass
+
+struct BoxArgs {
+  const unsigned char* ref;
+  const unsigned char* dist;
+  long long row_pitch_b, frame_pitch_b;
+  int dtype, esize;
+  int n, h, w;
+  int k, s, gh, gw;
+  int na;                     // anchor columns per strip (integer kernel)
+  int seg_anchors;            // anchor rows per segment (gridDim.y segments)
+  int ch;                     // staged input rows per chunk (multiple of s)
+  int in_pitch;               // staging row pitch, bytes
+  int nslot;                  // prefix history slots
+  double sscale1, sscale2;    // 2^-scale_log2, 2^-2*scale_log2 (exact rescaling of sums)
+  double area, inv_area;
+  int area_pow2;              // area is a power of two: x/area == x*inv_area exactly
+  double c1, c2;
+  int want;
+  double* partials;           // [n][gridDim.y][gridDim.x][3]
+  double* maps;               // float64 [n][planes][gh][gw]
+  long long map_plane, map_frame;
+  long long* wsums;           // optional int64 [n][5][gh][gw]
+};
+
+size_t box_smem_bytes(const BoxArgs& a, bool wide);
+int launch_box_int(const BoxArgs& a, dim3 grid, bool wide, cudaStream_t st);
+int launch_box_float(const BoxArgs& a, dim3 grid, dim3 block, cudaStream_t st);
+
+// ---------------- helpers ----------------
+int launch_reduce_partials(const double* partials, int nparts, int n, int ncomp, double mul,
+                           double* out, int out_stride, int out_offset, int comp_offset,
+                           cudaStream_t st);
+int launch_downsample(const unsigned char* src_r, const unsigned char* src_d, int src_dtype,
+                      long long src_rp, long long src_fp, int n, int h, int w,
+                      unsigned char* dst_r, unsigned char* dst_d, int dst_dtype, long long dst_rp,
+                      long long dst_fp, cudaStream_t st);
+int launch_integral(const unsigned char* ref, const unsigned char* dist, int dtype,
+                    long long rp, long long fp, int n, int h, int w, void* out, cudaStream_t st);
+
+}  // namespace ssk

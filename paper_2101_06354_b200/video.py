@@ -1,0 +1,200 @@
+"""Frame-sequence driver: pinned-host staging, async H2D, batched scoring.
+
+This is the B200 counterpart of the reference's frame loop
+(``run_score``, src/pipeline.py:275-366, optional ThreadPoolExecutor at
+:319-322) for the luma / multiscale / channel-wise color models: frames are
+packed into a pinned host ring (two slots), uploaded on a dedicated copy
+stream while the previous batch is being scored on the compute stream, and
+only per-frame scalars come back.  Results are in frame order, one record per
+frame with the pipeline's fields (score, am, l_mean, cs_mean;
+src/pipeline.py:57-58, :230-236), then pooled over time with the configured
+temporal pooler (src/pooling.py:246-280).
+
+Multi-GPU: ``shard_bounds`` splits frame indices into contiguous per-rank
+blocks (every frame pair is independent, so no collective is on the data
+path); ``gather_frame_scores`` concatenates the per-rank score vectors after
+scoring, in frame order.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+
+from . import _native as nat
+from . import batch as B
+from .errors import EmptySeries, ValidationError
+from .options import MultiscaleSpec, SsimConfig
+from .planes import ScoreSeries
+from .pooling import pool_temporal
+
+
+@dataclass
+class FrameRecord:
+    frame: int
+    score: float
+    am: Optional[float]
+    l_mean: Optional[float]
+    cs_mean: Optional[float]
+
+
+@dataclass
+class SequenceResult:
+    records: list = field(default_factory=list)
+    pooled: float = float("nan")
+    h2d_bytes: int = 0
+
+    @property
+    def scores(self) -> np.ndarray:
+        return np.array([r.score for r in self.records], dtype=np.float64)
+
+
+def shard_bounds(n_frames: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous block [start, stop) of frame indices owned by ``rank``."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValidationError(f"bad rank {rank} of {world}")
+    base, extra = divmod(n_frames, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def gather_frame_scores(local: np.ndarray, n_frames: int, group=None) -> np.ndarray:
+    """All ranks' per-frame scores concatenated in frame order (after scoring; off the hot path)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    counts = [shard_bounds(n_frames, r, world) for r in range(world)]
+    width = max(stop - start for start, stop in counts)
+    buf = torch.full((width,), float("nan"), dtype=torch.float64)
+    buf[: local.size] = torch.from_numpy(np.asarray(local, dtype=np.float64))
+    if dist.get_backend(group) == "nccl":
+        buf = buf.cuda()
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    out = [p.cpu().numpy()[: stop - start] for p, (start, stop) in zip(parts, counts)]
+    return np.concatenate(out)
+
+
+class SequenceScorer:
+    """Score a stream of frame pairs on one GPU.
+
+    ``color_weights`` (3-tuple) scores YCbCr frames given as (Y, Cb, Cr) plane
+    tuples with ``fixed_weight_cssim``; otherwise frames are luma planes.
+    ``config.multiscale`` enabled -> MS-SSIM per frame (score only, as in the
+    reference pipeline, src/pipeline.py:224-226).
+    """
+
+    def __init__(self, config: SsimConfig = SsimConfig(), batch_frames: int = 16,
+                 color_weights: Optional[Sequence[float]] = None, device=None):
+        self.config = config
+        self.batch_frames = max(1, int(batch_frames))
+        self.color_weights = tuple(color_weights) if color_weights is not None else None
+        self.device = device or nat.require_device()
+        torch = nat.torch_mod()
+        self.copy_stream = torch.cuda.Stream(device=self.device)
+        self._slots = [None, None]
+        self._events = [None, None]   # upload of the slot finished (host buffer reusable)
+        self._done = [None, None]     # scoring of the slot finished (device buffer reusable)
+
+    # -- staging ------------------------------------------------------------
+    def _stage(self, slot: int, frames: list):
+        """Pack a batch into pinned slot memory and upload it on the copy stream."""
+        torch = nat.torch_mod()
+        nplanes = 3 if self.color_weights is not None else 1
+        planes_ref, planes_dist = [], []
+        shapes = []
+        for p in range(nplanes):
+            r0 = np.asarray(frames[0][0][p] if nplanes == 3 else frames[0][0])
+            shapes.append((r0.shape, r0.dtype))
+        key = (len(frames), tuple(s for s, _ in shapes), tuple(str(d) for _, d in shapes))
+        slot_bufs = self._slots[slot]
+        if slot_bufs is None or slot_bufs[0] != key:
+            bufs = []
+            for (h, w), dt in shapes:
+                t_dt = torch.uint8 if dt == np.uint8 else torch.uint16
+                pitch = nat.aligned_pitch(w, nat.U8 if dt == np.uint8 else nat.U16)
+                host = torch.zeros((2, len(frames), h, pitch), dtype=t_dt, pin_memory=True)
+                dev = torch.empty_like(host, device=self.device)
+                bufs.append((host, dev, w))
+            slot_bufs = (key, bufs)
+            self._slots[slot] = slot_bufs
+        if self._events[slot] is not None:
+            self._events[slot].synchronize()  # host slot free again (its upload finished)
+        nbytes = 0
+        with torch.cuda.stream(self.copy_stream):
+            if self._done[slot] is not None:
+                self.copy_stream.wait_event(self._done[slot])
+            for p, (host, dev, w) in enumerate(slot_bufs[1]):
+                hv = host.numpy()
+                for i, (r, d) in enumerate(frames):
+                    hv[0, i, :, :w] = r[p] if nplanes == 3 else r
+                    hv[1, i, :, :w] = d[p] if nplanes == 3 else d
+                dev.copy_(host, non_blocking=True)
+                nbytes += host.numel() * host.element_size()
+                planes_ref.append(dev[0, :, :, :w])
+                planes_dist.append(dev[1, :, :, :w])
+            ev = torch.cuda.Event()
+            ev.record(self.copy_stream)
+        self._events[slot] = ev
+        return planes_ref, planes_dist, ev, nbytes
+
+    def _score_batch(self, planes_ref, planes_dist):
+        cfg = self.config
+        if self.color_weights is not None:
+            return B.color_batch(planes_ref, planes_dist, cfg, weights=self.color_weights), None
+        if cfg.multiscale.enabled:
+            return B.msssim_batch(planes_ref[0], planes_dist[0], cfg, cfg.multiscale), None
+        terms = B.ssim_terms_batch(planes_ref[0], planes_dist[0], cfg)
+        return terms.score, terms
+
+    def score(self, ref_frames: Iterable, dist_frames: Iterable) -> SequenceResult:
+        torch = nat.torch_mod()
+        result = SequenceResult()
+        pending = []
+        batch: list = []
+        slot = 0
+        compute = torch.cuda.current_stream(self.device)
+
+        def flush(frames):
+            nonlocal slot
+            pr, pd, ev, nbytes = self._stage(slot, frames)
+            result.h2d_bytes += nbytes
+            compute.wait_event(ev)
+            score, terms = self._score_batch(pr, pd)
+            done = torch.cuda.Event()
+            done.record(compute)
+            self._done[slot] = done
+            pending.append((len(frames), score, terms))
+            slot ^= 1
+
+        for r, d in zip(ref_frames, dist_frames):
+            batch.append((r, d))
+            if len(batch) == self.batch_frames:
+                flush(batch)
+                batch = []
+        if batch:
+            flush(batch)
+        idx = 0
+        for count, score, terms in pending:
+            s = score.cpu().numpy()
+            if terms is not None:
+                lm, cm = terms.l_mean.cpu().numpy(), terms.cs_mean.cpu().numpy()
+            for i in range(count):
+                if terms is not None:
+                    result.records.append(FrameRecord(idx, float(s[i]), float(s[i]), float(lm[i]), float(cm[i])))
+                else:
+                    result.records.append(FrameRecord(idx, float(s[i]), None, None, None))
+                idx += 1
+        if not result.records:
+            raise EmptySeries("no frames to score")
+        result.pooled = pool_temporal(ScoreSeries(result.scores), self.config.temporal_pool)
+        return result
+
+
+def score_sequence(ref_frames, dist_frames, config: SsimConfig = SsimConfig(), batch_frames: int = 16,
+                   color_weights=None) -> SequenceResult:
+    """Convenience wrapper around ``SequenceScorer``."""
+    return SequenceScorer(config, batch_frames, color_weights).score(ref_frames, dist_frames)

@@ -1,0 +1,286 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against golden vectors and the oracle.
+
+Tolerances (north star, BASELINE.json): integer window sums bit-exact; rect
+windows on integer samples also give bit-exact maps (float64 epilogue in the
+reference's operation order); Gaussian windows run in fp32 with maps within
+1e-4 and per-frame scores within 1e-5 absolute of the float64 reference.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2101_06354_b200 as P
+from paper_2101_06354_b200 import engine
+from paper_2101_06354_b200.errors import (
+    BitDepthMismatch,
+    DimensionMismatch,
+    EngineShapeMismatch,
+    TooManyLevels,
+    TooSmall,
+    ValidationError,
+    WindowLargerThanImage,
+)
+
+pytestmark = pytest.mark.gpu
+
+MAP_TOL = 1e-4
+SCORE_TOL = 1e-5
+
+CASES = {
+    "gauss11": (P.SsimConfig(window=P.WindowSpec.gaussian(1.5)), 8, False),
+    "gauss_s3": (P.SsimConfig(window=P.WindowSpec.gaussian(1.5, stride=3)), 8, False),
+    "gauss13_10b": (P.SsimConfig(bit_depth=10, window=P.WindowSpec.gaussian(2.0)), 10, False),
+    "rect11": (P.SsimConfig(), 8, True),
+    "rect8s4_10b": (P.SsimConfig(bit_depth=10, window=P.WindowSpec.rectangular(8, stride=4), engine="integral"), 10, True),
+    "rect11_16b": (P.SsimConfig(bit_depth=16), 16, True),
+    "rect1": (P.SsimConfig(window=P.WindowSpec.rectangular(1), engine="naive"), 8, True),
+    "rect16": (P.SsimConfig(window=P.WindowSpec.rectangular(16), engine="naive"), 8, True),
+    "rect5_float": (P.SsimConfig(window=P.WindowSpec.rectangular(5)), 8, False),
+}
+
+
+def planes(golden, name, bd):
+    return P.LumaPlane(golden[f"{name}/ref"], bd), P.LumaPlane(golden[f"{name}/dist"], bd)
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_maps_against_golden(cuda, golden, name):
+    cfg, bd, exact = CASES[name]
+    a, b = planes(golden, name, bd)
+    maps = P.ssim_map(a, b, cfg)
+    for key, got in (("l", maps.l_map.values), ("cs", maps.cs_map.values), ("q", maps.q_map.values)):
+        want = golden[f"{name}/{key}"]
+        assert got.shape == want.shape
+        if exact:
+            assert np.array_equal(got, want), f"{name}/{key} not bit-exact"
+        else:
+            assert np.max(np.abs(got - want)) < MAP_TOL, f"{name}/{key}"
+    assert abs(P.ssim_score(a, b, cfg) - float(golden[f"{name}/score"])) < SCORE_TOL
+    q, lm, cm = P.ssim_terms(a, b, cfg)
+    assert np.max(np.abs(np.array([q, lm, cm]) - golden[f"{name}/terms"])) < SCORE_TOL
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_local_statistics_against_golden(cuda, golden, name):
+    cfg, bd, exact = CASES[name]
+    a, b = planes(golden, name, bd)
+    st = P.local_statistics(a, b, cfg.window, cfg.engine)
+    got = np.stack([st.mu1, st.mu2, st.var1, st.var2, st.cov])
+    want = golden[f"{name}/stats"]
+    if exact:
+        assert np.array_equal(got, want)
+    else:
+        scale = max(1.0, float(np.abs(want).max()))
+        assert np.max(np.abs(got - want)) / scale < 1e-5
+    assert st.grid_shape == want.shape[1:]
+    assert st.stride == cfg.window.stride and st.window_size == cfg.window.k
+
+
+@pytest.mark.parametrize("name,k,s,bd", [("rect8s4_10b", 8, 4, 10), ("rect11_16b", 11, 1, 16)])
+def test_integer_window_sums_bit_exact(cuda, golden, name, k, s, bd):
+    pair = engine.upload_pair(golden[f"{name}/ref"], golden[f"{name}/dist"], bd, gauss=False)
+    got = engine.window_sums(pair, k, s)[0].cpu().numpy()
+    assert np.array_equal(got, golden[f"{name}/wsums"])
+
+
+def test_integral_set_and_window_sum(cuda, golden):
+    iset = P.build_integral_set(P.LumaPlane(golden["sat/ref"]), P.LumaPlane(golden["sat/dist"]))
+    got = np.stack([iset.table(t) for t in ("sum1", "sum2", "sq1", "sq2", "prod")])
+    assert got.dtype == np.int64 and np.array_equal(got, golden["sat/tables"])
+    a = golden["sat/ref"].astype(np.int64)
+    assert P.window_sum(iset, "sum1", 1, 1, 3) == a[1:4, 1:4].sum()
+
+
+def test_dyadic_downsample_exact(cuda, golden):
+    out = P.dyadic_downsample(P.LumaPlane(golden["down/in"]))
+    assert isinstance(out, P.LumaPlane)
+    assert np.array_equal(out.samples, golden["down/out"])
+    raw = P.dyadic_downsample(golden["down/in"].astype(np.float64) / 3.0)
+    assert np.array_equal(raw, golden["down/out"] / 3.0) or np.max(np.abs(raw - golden["down/out"] / 3.0)) < 1e-13
+    with pytest.raises(TooSmall):
+        P.dyadic_downsample(np.zeros((1, 8), dtype=np.uint8))
+
+
+def test_msssim_against_golden(cuda, golden):
+    a, b = P.LumaPlane(golden["ms_gauss/ref"]), P.LumaPlane(golden["ms_gauss/dist"])
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    levels = P.scale_scores(a, b, cfg, 5)
+    assert np.max(np.abs(np.array(levels) - golden["ms_gauss/levels"])) < SCORE_TOL
+    assert abs(P.msssim(a, b, cfg, P.MultiscaleSpec.product(5)) - float(golden["ms_gauss/score"])) < SCORE_TOL
+    a, b = P.LumaPlane(golden["ms_rect5/ref"]), P.LumaPlane(golden["ms_rect5/dist"])
+    cfg = P.SsimConfig(window=P.WindowSpec.rectangular(5))
+    levels = P.scale_scores(a, b, cfg, 4)
+    assert np.max(np.abs(np.array(levels) - golden["ms_rect5/levels4"])) < 1e-12  # exact pyramid + fp64
+    assert abs(P.msssim(a, b, cfg, P.MultiscaleSpec("sum", 3, (0.2, 0.3, 0.5))) - float(golden["ms_rect5/sum3"])) < 1e-12
+    assert abs(P.msssim(a, b, cfg, P.MultiscaleSpec.fast4()) - float(golden["ms_rect5/fast4"])) < 1e-12
+
+
+def test_color_against_golden(cuda, golden):
+    ref = P.ColorFrame(tuple(golden[f"color/ref{i}"] for i in range(3)), "ycbcr-bt709", "420")
+    dist = P.ColorFrame(tuple(golden[f"color/dist{i}"] for i in range(3)), "ycbcr-bt709", "420")
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    assert abs(P.fixed_weight_cssim(ref, dist, (4 / 6, 1 / 6, 1 / 6), cfg) - float(golden["color/fixed"])) < SCORE_TOL
+    assert abs(P.channelwise_cssim(ref, dist, -0.3, -0.3, cfg) - float(golden["color/cw"])) < SCORE_TOL
+    per = np.array(P.channel_scores(ref, dist, cfg))
+    assert np.max(np.abs(per - golden["color/per_plane"])) < SCORE_TOL
+    # (1, 0, 0) weights reduce to the luma score exactly (tests/test_color.py:109-114)
+    assert P.fixed_weight_cssim(ref, dist, (1.0, 0.0, 0.0), cfg) == P.ssim_score(ref.channels[0], dist.channels[0], cfg)
+
+
+def test_config1_score(cuda, golden):
+    from paper_2101_06354_b200 import synth
+
+    a, b = synth.config1_pair()
+    terms = P.ssim_terms(P.LumaPlane(a), P.LumaPlane(b), P.SsimConfig(window=P.WindowSpec.gaussian(1.5)))
+    assert np.max(np.abs(np.array(terms) - golden["config1/terms"])) < SCORE_TOL
+
+
+# --- properties the reference's tests pin -----------------------------------
+
+@pytest.mark.parametrize("cfg", [P.SsimConfig(), P.SsimConfig(window=P.WindowSpec.gaussian(1.5)),
+                                 P.SsimConfig(window=P.WindowSpec.rectangular(8, stride=3))])
+def test_symmetry_exact(cuda, rng, cfg):
+    a = rng.integers(0, 256, (45, 53)).astype(np.uint8)
+    b = np.clip(a.astype(int) + rng.integers(-25, 26, a.shape), 0, 255).astype(np.uint8)
+    fwd, rev = P.ssim_map(a, b, cfg), P.ssim_map(b, a, cfg)
+    for attr in ("l_map", "cs_map", "q_map"):
+        assert np.array_equal(getattr(fwd, attr).values, getattr(rev, attr).values)
+    assert P.ssim_score(a, b, cfg) == P.ssim_score(b, a, cfg)
+
+
+@pytest.mark.parametrize("window", [P.WindowSpec.rectangular(11, stride=5), P.WindowSpec.rectangular(11, stride=3),
+                                    P.WindowSpec.gaussian(1.5, stride=4), P.WindowSpec.gaussian(1.5, stride=2),
+                                    P.WindowSpec.rectangular(8, stride=4)])
+def test_stride_is_exact_subsample(cuda, rng, window):
+    a = rng.integers(0, 256, (48, 40)).astype(np.uint8)
+    b = rng.integers(0, 256, (48, 40)).astype(np.uint8)
+    s = window.stride
+    strided = P.local_statistics(a, b, window)
+    dense = P.local_statistics(a, b, window.with_stride(1))
+    for name in ("mu1", "mu2", "var1", "var2", "cov"):
+        assert np.array_equal(getattr(strided, name), getattr(dense, name)[::s, ::s])
+
+
+@pytest.mark.parametrize("cfg", [P.SsimConfig(), P.SsimConfig(window=P.WindowSpec.gaussian(1.5))])
+def test_identity_and_bounds(cuda, rng, cfg):
+    a = rng.integers(0, 256, (40, 40)).astype(np.uint8)
+    b = rng.integers(0, 256, (40, 40)).astype(np.uint8)
+    tol = 1e-12 if cfg.window.shape == "rect" else 1e-6
+    assert abs(P.ssim_score(a, a, cfg) - 1.0) < tol
+    q = P.ssim_map(a, b, cfg).q_map.values
+    assert np.all(np.abs(q) <= 1.0 + 1e-6)
+    c = a.copy()
+    c[7, 9] = c[7, 9] + 1 if c[7, 9] < 255 else c[7, 9] - 1
+    assert P.ssim_score(a, c, cfg) < 1.0 - 1e-9
+
+
+def test_delta_kernel_reproduces_input(cuda, rng):
+    a = rng.integers(0, 256, (12, 12)).astype(np.uint8)
+    b = rng.integers(0, 256, (12, 12)).astype(np.uint8)
+    st = P.local_statistics(P.LumaPlane(a), P.LumaPlane(b), P.WindowSpec.gaussian(0.01), "naive")
+    assert np.array_equal(st.mu1, a[1:-1, 1:-1].astype(float))
+    assert np.array_equal(st.mu2, b[1:-1, 1:-1].astype(float))
+
+
+@pytest.mark.parametrize("h,w,k", [(11, 11, 11), (11, 300, 11), (300, 11, 11), (13, 17, 3), (129, 131, 7),
+                                   (257, 130, 11), (5, 5, 1), (64, 129, 15)])
+def test_edge_geometries_vs_oracle(cuda, oracle, rng, h, w, k):
+    a = rng.integers(0, 256, (h, w)).astype(np.uint8)
+    b = np.clip(a.astype(int) + rng.integers(-30, 31, a.shape), 0, 255).astype(np.uint8)
+    want = oracle.ssim_maps(a, b, shape="rect", k=k)
+    got = P.ssim_map(a, b, P.SsimConfig(window=P.WindowSpec.rectangular(k)))
+    assert np.array_equal(got.q_map.values, want[2])
+    if k >= 3 and k % 2 == 1:
+        want = oracle.ssim_maps(a, b, shape="gauss", k=k, sigma=k / 6.0)
+        got = P.ssim_map(a, b, P.SsimConfig(window=P.WindowSpec.gaussian(k / 6.0, k=k)))
+        assert np.max(np.abs(got.q_map.values - want[2])) < MAP_TOL
+
+
+def test_errors_match_reference_classes(cuda, rng):
+    a = rng.integers(0, 256, (8, 8)).astype(np.uint8)
+    with pytest.raises(WindowLargerThanImage):
+        P.ssim_map(a, a)  # rect 11 on 8x8
+    with pytest.raises(EngineShapeMismatch):
+        P.local_statistics(a, a, P.WindowSpec.gaussian(0.5), "integral")
+    with pytest.raises(DimensionMismatch):
+        P.ssim_score(a, a[:7])
+    with pytest.raises(BitDepthMismatch):
+        P.ssim_score(P.LumaPlane(a, 8), P.LumaPlane(a.astype(np.uint16), 10))
+    big = rng.integers(0, 256, (32, 32)).astype(np.uint8)
+    with pytest.raises(TooManyLevels):
+        P.msssim(big, big, P.SsimConfig(window=P.WindowSpec.rectangular(5)), P.MultiscaleSpec.product(4))
+    with pytest.raises(ValidationError):
+        P.msssim(big, big, P.SsimConfig(window=P.WindowSpec.rectangular(5)), P.MultiscaleSpec.off())
+    with pytest.raises(ValidationError):
+        P.local_statistics(big, big, P.WindowSpec.rectangular(5), "fast")
+
+
+# --- batched device API and full-size configurations -------------------------
+
+def test_batch_matches_per_pair(cuda, rng):
+    import torch
+
+    n, h, w = 5, 70, 90
+    a = rng.integers(0, 256, (n, h, w)).astype(np.uint8)
+    b = np.clip(a.astype(int) + rng.integers(-20, 21, a.shape), 0, 255).astype(np.uint8)
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    got = P.ssim_batch(ta, tb, cfg).cpu().numpy()
+    want = np.array([P.ssim_score(a[i], b[i], cfg) for i in range(n)])
+    assert np.array_equal(got, want)
+    ms, terms = P.msssim_batch(ta, tb, cfg, P.MultiscaleSpec.product(2), with_ssim=True)
+    assert np.array_equal(terms.score.cpu().numpy(), want)
+    want_ms = [P.msssim(a[i], b[i], cfg, P.MultiscaleSpec.product(2)) for i in range(n)]
+    assert np.max(np.abs(ms.cpu().numpy() - np.array(want_ms))) < 1e-12
+    # determinism: bit-identical on a rerun
+    assert np.array_equal(P.ssim_batch(ta, tb, cfg).cpu().numpy(), got)
+
+
+def test_full_1080p_gauss_ssim_and_msssim(cuda, oracle):
+    from paper_2101_06354_b200 import synth
+
+    a, b = synth.dct_pair(2, 0)
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    win = dict(shape="gauss", k=11, sigma=1.5)
+    terms = P.ssim_terms(a, b, cfg)
+    assert np.max(np.abs(np.array(terms) - np.array(oracle.ssim_terms(a, b, **win)))) < SCORE_TOL
+    got = P.scale_scores(a, b, cfg, 5)
+    want = oracle.scale_scores(a, b, 5, **win)
+    assert np.max(np.abs(np.array(got) - np.array(want))) < SCORE_TOL
+    maps = P.ssim_map(a, b, cfg)
+    wl, wcs, wq = oracle.ssim_maps(a, b, **win)
+    assert np.max(np.abs(maps.q_map.values - wq)) < MAP_TOL
+    assert np.max(np.abs(maps.cs_map.values - wcs)) < MAP_TOL
+
+
+def test_full_4k_10bit_box_sums_bit_exact(cuda, oracle):
+    from paper_2101_06354_b200 import synth
+
+    a, b = synth.config4_pair(0)
+    pair = engine.upload_pair(a, b, 10, gauss=False)
+    got = engine.window_sums(pair, 8, 4)[0].cpu().numpy()
+    want = oracle.box_window_sums(a, b, 8, 4)
+    assert got.shape == (5, 539, 959)
+    assert np.array_equal(got, want)
+    cfg = P.SsimConfig(bit_depth=10, window=P.WindowSpec.rectangular(8, stride=4), engine="integral")
+    q = P.ssim_map(P.LumaPlane(a, 10), P.LumaPlane(b, 10), cfg).q_map.values
+    assert np.array_equal(q, oracle.ssim_maps(a, b, shape="rect", k=8, stride=4, bit_depth=10)[2])
+
+
+def test_video_sequence_yuv420(cuda, oracle):
+    from paper_2101_06354_b200 import synth
+
+    vid = synth.VideoConfig3(frames=6, h=64, w=96)
+    pairs = [vid.pair(t) for t in range(6)]
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    wts = (4 / 6, 1 / 6, 1 / 6)
+    res = P.score_sequence([r for r, _ in pairs], [d for _, d in pairs], cfg, batch_frames=4, color_weights=wts)
+    win = dict(shape="gauss", k=11, sigma=1.5)
+    want = [oracle.fixed_weight(oracle.channel_scores(r, d, **win), wts) for r, d in pairs]
+    assert np.max(np.abs(res.scores - np.array(want))) < SCORE_TOL
+    assert abs(res.pooled - oracle.pool_temporal_am(want)) < SCORE_TOL
+    # luma records carry (score, am, l_mean, cs_mean)
+    luma = P.score_sequence([r[0] for r, _ in pairs], [d[0] for _, d in pairs], cfg, batch_frames=4)
+    for rec, (r, d) in zip(luma.records, pairs):
+        assert np.max(np.abs(np.array([rec.score, rec.l_mean, rec.cs_mean]) -
+                             np.array(oracle.ssim_terms(r[0], d[0], **win)))) < SCORE_TOL

@@ -1,0 +1,95 @@
+"""The C-ABI library loads without a GPU and exports exactly what include/ssimk.h declares."""
+
+import ctypes
+import re
+import shutil
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from paper_2101_06354_b200 import _native as nat
+
+REPO = Path(__file__).resolve().parents[1]
+HEADER = REPO / "include" / "ssimk.h"
+
+
+def declared_functions():
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    return sorted(set(re.findall(r"\b(ssk_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = nat.load_library()
+    names = declared_functions()
+    assert names, "no declarations parsed"
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing
+    assert sorted(nat.EXPORTED_SYMBOLS) == names
+    # the symbols must be exported with C linkage (no mangling)
+    nm = shutil.which("nm")
+    if nm:
+        out = subprocess.run([nm, "-D", "--defined-only", str(nat.LIB_PATH)], capture_output=True, text=True).stdout
+        exported = set(re.findall(r"\bT (ssk_\w+)", out))
+        assert set(names) <= exported
+
+
+def test_abi_version_and_errors():
+    lib = nat.load_library()
+    assert lib.ssk_abi_version() == nat.ABI_VERSION
+    assert lib.ssk_strerror(0) == b"ok"
+    assert b"window" in lib.ssk_strerror(nat.E_WINDOW)
+    assert lib.ssk_strerror(-99) == b"unknown error"
+
+
+def test_argument_errors_need_no_gpu():
+    """Validation happens before any launch, so bad calls fail cleanly even on a CPU host."""
+    lib = nat.load_library()
+    assert lib.ssk_ssim(None, None, 1, None, None, None, 0, None) == nat.E_ARG
+    p = nat.Planes(ref=16, dist=32, dtype=nat.U8, n=1, h=8, w=8, bit_depth=8, row_pitch=16, frame_pitch=128)
+    win = nat.Window(shape=nat.RECT, k=11, stride=1, c1=1.0, c2=1.0)
+    sums = ctypes.c_void_p(64)
+    assert lib.ssk_ssim(ctypes.byref(p), ctypes.byref(win), 1, sums, None, None, 0, None) == nat.E_WINDOW
+    win.k = 4
+    assert lib.ssk_ssim(ctypes.byref(p), ctypes.byref(win), 1, sums, None, None, 0, None) == nat.E_WORKSPACE
+    p.ref = 17  # misaligned
+    assert lib.ssk_ssim(ctypes.byref(p), ctypes.byref(win), 1, sums, None, None, 0, None) == nat.E_ALIGN
+    p.ref = 16
+    win.shape, win.k = nat.GAUSS, 4  # even Gaussian window
+    assert lib.ssk_ssim(ctypes.byref(p), ctypes.byref(win), 1, sums, None, None, 0, None) == nat.E_SHAPE
+    assert lib.ssk_ssim_workspace_bytes(ctypes.byref(p), ctypes.byref(win)) == 0
+    win.shape, win.k = nat.RECT, 3
+    assert lib.ssk_ssim_workspace_bytes(ctypes.byref(p), ctypes.byref(win)) > 0
+    means = ctypes.c_void_p(64)
+    assert lib.ssk_msssim(ctypes.byref(p), ctypes.byref(win), 3, means, None, None, 0, None) == nat.E_LEVELS
+
+
+def test_error_codes_map_to_reference_exceptions():
+    from paper_2101_06354_b200 import errors
+
+    with pytest.raises(errors.WindowLargerThanImage):
+        nat.raise_for(nat.E_WINDOW)
+    with pytest.raises(errors.TooManyLevels):
+        nat.raise_for(nat.E_LEVELS)
+    with pytest.raises(errors.TooSmall):
+        nat.raise_for(nat.E_TOO_SMALL)
+    with pytest.raises(errors.ValidationError):
+        nat.raise_for(nat.E_ARG)
+
+
+@pytest.mark.skipif(shutil.which("gcc") is None, reason="needs gcc")
+def test_ctypes_struct_layout_matches_header(tmp_path):
+    src = tmp_path / "layout.c"
+    src.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "ssimk.h"\n'
+        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu\\n\", sizeof(ssk_planes), offsetof(ssk_planes,row_pitch),"
+        " offsetof(ssk_planes,frame_pitch), sizeof(ssk_window), offsetof(ssk_window,c1), offsetof(ssk_window,taps));"
+        "return 0;}\n"
+    )
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", str(REPO / "include"), str(src), "-o", str(exe)], check=True)
+    vals = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert vals == [
+        ctypes.sizeof(nat.Planes), nat.Planes.row_pitch.offset, nat.Planes.frame_pitch.offset,
+        ctypes.sizeof(nat.Window), nat.Window.c1.offset, nat.Window.taps.offset,
+    ]
