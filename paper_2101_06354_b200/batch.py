@@ -45,7 +45,7 @@ def ssim_terms_batch(ref, dist, config: SsimConfig = SsimConfig(), stream=None) 
     sums, _ = engine.ssim(pair, config.window, config.c1, config.c2,
                           nat.WANT_Q | nat.WANT_L | nat.WANT_CS, stream)
     gh, gw = engine.grid_shape(h, w, config.window.k, config.window.stride)
-    means = sums / float(gh * gw)
+    means = engine.frame_means(sums, gh * gw)
     return FrameTerms(means[:, 0], means[:, 1], means[:, 2])
 
 
@@ -84,7 +84,7 @@ def msssim_batch(ref, dist, config: SsimConfig = SsimConfig(), spec: Optional[Mu
     if not with_ssim:
         return score
     gh, gw = engine.grid_shape(h, w, k, config.window.stride)
-    m = ssim_sums / float(gh * gw)
+    m = engine.frame_means(ssim_sums, gh * gw)
     return score, FrameTerms(m[:, 0], m[:, 1], m[:, 2])
 
 

@@ -9,12 +9,13 @@ namespace ssk {
 
 // ---------------------------------------------------------------------------
 // Fold per-CTA partials [n][nparts][ncomp] into out[f*out_stride + out_offset + c]
-// = mul * sum_p partials[f][p][comp_offset + c]; one warp per frame, fixed
+// = (sum_p partials[f][p][comp_offset + c]) / divisor (IEEE division, so a
+// mean is rounded exactly like numpy's sum/count); one warp per frame, fixed
 // order -> bit-reproducible run to run (the reference's ordered frame results,
 // tests/test_cli.py:124-130, rely on determinism).
 // ---------------------------------------------------------------------------
 __global__ void reduce_partials_kernel(const double* __restrict__ partials, int nparts, int n,
-                                       int ncomp, double mul, double* __restrict__ out,
+                                       int ncomp, double divisor, double* __restrict__ out,
                                        int out_stride, int out_offset, int comp_offset) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -24,16 +25,16 @@ __global__ void reduce_partials_kernel(const double* __restrict__ partials, int 
     double s = 0.0;
     for (int i = lane; i < nparts; i += 32) s += p[(long long)i * 3 + comp_offset + c];
     s = warp_sum(s);
-    if (lane == 0) out[(long long)warp * out_stride + out_offset + c] = s * mul;
+    if (lane == 0) out[(long long)warp * out_stride + out_offset + c] = divisor == 1.0 ? s : __ddiv_rn(s, divisor);
   }
 }
 
-int launch_reduce_partials(const double* partials, int nparts, int n, int ncomp, double mul,
+int launch_reduce_partials(const double* partials, int nparts, int n, int ncomp, double divisor,
                            double* out, int out_stride, int out_offset, int comp_offset,
                            cudaStream_t st) {
   const int threads = 256;
   const int blocks = (n * 32 + threads - 1) / threads;
-  reduce_partials_kernel<<<blocks, threads, 0, st>>>(partials, nparts, n, ncomp, mul, out,
+  reduce_partials_kernel<<<blocks, threads, 0, st>>>(partials, nparts, n, ncomp, divisor, out,
                                                      out_stride, out_offset, comp_offset);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;

@@ -90,7 +90,6 @@ __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_consta
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double s_red[(BX_THREADS / 32) * 3];
   const int CH = a.ch, s = a.s, k = a.k, P = a.in_pitch, NSL = a.nslot;
-  const int VR = CH / s;
   constexpr int VP = BX_THREADS + 4;
   unsigned char* stage = smem;                                            // [2][2][CH][P]
   ACC* hist = reinterpret_cast<ACC*>(smem + (size_t)4 * CH * P);          // [NSL][5][128]
@@ -99,7 +98,9 @@ __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_consta
   const int tid = threadIdx.x;
   const int strip = blockIdx.x, seg = blockIdx.y, frame = blockIdx.z;
   const int A0 = strip * a.na;
-  const int c0 = A0 * s;
+  // stage from a 16-byte aligned column; anchors sit `delta` columns into the stage
+  const int c0 = (A0 * s) & ~((16 / (int)sizeof(TIN)) - 1);
+  const int delta = A0 * s - c0;
   const int b0 = seg * a.seg_anchors;
   const int b1 = min(b0 + a.seg_anchors, a.gh);
   const int r0 = b0 * s;
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_consta
       const int ac = A0 + jj;
       const int ar = b0 + bfirst + g;
       if (ac >= a.gw || ar >= b1) continue;
-      const ACC* vr = vrow + (size_t)g * 5 * VP + jj * s;
+      const ACC* vr = vrow + (size_t)g * 5 * VP + jj * s + delta;
       ACC sums[5];
 #pragma unroll
       for (int m = 0; m < 5; ++m) {

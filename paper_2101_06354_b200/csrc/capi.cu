@@ -85,16 +85,13 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
     a.gh = pl.gh;
     a.gw = pl.gw;
     a.stride = s;
-    const int nstrips = (a.wo + GS_TW - 1) / GS_TW;
-    const long long target = 2368;  // >= 4 waves of 148 SMs x 4 resident CTAs
+    const int nstrips = (a.wo + gauss_tw(k) - 1) / gauss_tw(k);
+    // Segments depend on the frame geometry only (never on the batch size), so a
+    // frame's fp32 partial sums -- and hence its score -- are bit-identical
+    // however frames are batched or sharded.
     int nseg = (a.ho + 127) / 128;
-    const long long want_seg = (target + (long long)nstrips * p->n - 1) / ((long long)nstrips * p->n);
-    const int max_seg = (a.ho + 31) / 32;
-    if (want_seg > nseg) nseg = (int)(want_seg < max_seg ? want_seg : max_seg);
-    if (nseg < 1) nseg = 1;
     a.seg_rows = (a.ho + nseg - 1) / nseg;
     nseg = (a.ho + a.seg_rows - 1) / a.seg_rows;
-    a.in_pitch = gauss_in_pitch(k, es);
     const float shift = (float)std::ldexp(1.0, p->bit_depth - 1);
     const double scale = std::ldexp(1.0, -p->scale_log2);
     a.conv_scale = (p->dtype == SSK_F32) ? 1.0f : (float)scale;
@@ -107,7 +104,7 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
     a.c2 = (float)win->c2;
     a.want = want;
     std::memcpy(a.taps, win->taps, sizeof(a.taps));
-    pl.grid = dim3(nstrips, nseg, p->n);
+    pl.grid = dim3(nstrips, nseg, (p->n + 1) / 2);  // two frames per CTA (packed fp32 pairs)
     pl.nparts_per_frame = (size_t)nstrips * nseg;
     a.map_plane = (long long)pl.gh * pl.gw;
     a.map_frame = a.map_plane * ((want & SSK_MAP_STATS) ? 5 : 3);
@@ -145,31 +142,25 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
   if (integer && k <= BX_THREADS) {
     pl.box_int = true;
     pl.wide = (double)k * k * stored_max * stored_max >= 4294967296.0;
-    a.na = (BX_THREADS - k) / s + 1;
-    const int nstrips = (pl.gw + a.na - 1) / a.na;
+    const int max_delta = 16 / es - 1;  // strips stage from a 16-byte aligned column
+    a.na = (BX_THREADS - max_delta - k) / s + 1;
+    const int nstrips = a.na > 0 ? (pl.gw + a.na - 1) / a.na : 0;
     int vr = 32 / s;
     vr = vr < 1 ? 1 : (vr > 8 ? 8 : vr);
     a.ch = vr * s;
     a.in_pitch = BX_THREADS * es + 16;
     a.nslot = (k + s - 1) / s + 1;
+    // geometry-only segmentation (~256 input rows), independent of the batch size
     int seg_anchors = (256 + s - 1) / s;
     if (seg_anchors < 1) seg_anchors = 1;
-    // enough CTAs for small batches: split rows further (down to ~32 input rows)
-    const long long target = 2368;
     long long nseg = (pl.gh + seg_anchors - 1) / seg_anchors;
-    const long long have = (long long)nstrips * p->n * nseg;
-    if (have < target) {
-      const int min_anchors = (32 + s - 1) / s;
-      long long want_seg = (target + (long long)nstrips * p->n - 1) / ((long long)nstrips * p->n);
-      int sa = (int)((pl.gh + want_seg - 1) / want_seg);
-      seg_anchors = sa < min_anchors ? min_anchors : sa;
-    }
+    seg_anchors = (int)((pl.gh + nseg - 1) / nseg);
     a.seg_anchors = seg_anchors;
     nseg = (pl.gh + seg_anchors - 1) / seg_anchors;
     if (nseg > 65535) return SSK_E_ARG;
     pl.grid = dim3(nstrips, (unsigned)nseg, p->n);
     pl.nparts_per_frame = (size_t)nstrips * nseg;
-    if (box_smem_bytes(a, pl.wide) > 227 * 1024) {
+    if (a.na < 1 || box_smem_bytes(a, pl.wide) > 227 * 1024) {
       pl.box_int = false;  // extreme strides: fall through to the direct kernel
     } else {
       return SSK_OK;
@@ -379,8 +370,8 @@ int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, double* d
     part_off += partial_bytes(pl, p->n);
     rc = run_plan(pl, partials, nullptr, nullptr, st);
     if (rc) return rc;
-    const double inv_count = 1.0 / ((double)pl.gh * (double)pl.gw);
-    rc = launch_reduce_partials(partials, (int)pl.nparts_per_frame, p->n, 1, inv_count,
+    const double count = (double)pl.gh * (double)pl.gw;
+    rc = launch_reduce_partials(partials, (int)pl.nparts_per_frame, p->n, 1, count,
                                 d_level_means, levels, l, last ? 0 : 2, st);
     if (rc) return rc;
     if (l == 0 && d_ssim_sums) {

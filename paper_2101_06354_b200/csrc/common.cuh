@@ -47,7 +47,8 @@ __device__ __forceinline__ double warp_sum(double v) {
 template <int NV, int NWARPS>
 __device__ __forceinline__ void block_sum_store(double (&v)[NV], double* scratch /*NWARPS*NV*/,
                                                 double* out /*NV*/) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;  // 1-D or 2-D blocks
+  const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
   for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
   if (lane == 0) {
@@ -55,11 +56,11 @@ __device__ __forceinline__ void block_sum_store(double (&v)[NV], double* scratch
     for (int i = 0; i < NV; ++i) scratch[warp * NV + i] = v[i];
   }
   __syncthreads();
-  if (threadIdx.x < NV) {
+  if (tid < NV) {
     double s = 0.0;
 #pragma unroll
-    for (int wi = 0; wi < NWARPS; ++wi) s += scratch[wi * NV + threadIdx.x];
-    out[threadIdx.x] = s;
+    for (int wi = 0; wi < NWARPS; ++wi) s += scratch[wi * NV + tid];
+    out[tid] = s;
   }
 }
 

@@ -1,0 +1,365 @@
+// K1: fused Gaussian-window local moments + SSIM terms + mean-pooling reduction.
+//
+// Replaces, for Gaussian windows, the reference's
+//   _sliding_weighted_sums x5   (src/stats.py:155-164, called at :247-255)
+//   stats_from_sums(area=1)     (src/stats.py:185-202)
+//   term_maps_from_stats        (src/ssim.py:31-46)
+//   mssim / pool_spatial("am")  (src/ssim.py:55-65, src/pooling.py:218-219)
+// The 2-D kernel outer(g,g)/sum (src/stats.py:41-44) is applied separably
+// with the normalised 1-D taps g/sum(g) (identical up to rounding;
+// tests/test_stats.py:126-129 pins separability).
+//
+// Blackwell design.  One CTA = 128 threads = a strip of TW output columns
+// (TW + K - 1 <= 128 input columns) of a segment of output rows, for TWO
+// frames at once: every value is carried as a packed fp32 pair (frame f,
+// frame f+1), so the whole filter runs on FFMA2 / FMUL2 / FADD2 -- two FMAs
+// per lane per issued instruction -- without any register shuffling (the
+// pairing is across frames, which share all addresses and weights).
+//   stage  : cp.async 16-B copies of G new input rows of the 4 images
+//            (ref/dist x 2 frames) into a ring of 2G+K-1 raw rows, one chunk
+//            ahead of the compute (double buffering), zero fill past the edge.
+//   V pass : thread = input column; converts samples exactly to fp32 (u8/u16
+//            via the 2^23-mantissa splice), subtracts the symmetric shift L/2
+//            (keeps E[x^2]-E[x]^2 well conditioned in fp32 and preserves exact
+//            ref/dist symmetry), forms x, y, x^2, y^2, xy and gathers the
+//            K-tap vertical filter for G output rows (5*G packed accumulators).
+//   H pass : thread = (output row, 8 adjacent columns); K-tap horizontal filter
+//            from the shared-memory V rows, then the SSIM epilogue on packed
+//            pairs, optional map stores and per-frame fp64 partial sums.
+//   reduce : warp-shuffle + shared-memory block reduction into one fp64
+//            partial per (frame, CTA); a second tiny kernel folds the partials
+//            per frame in a fixed order (bit-reproducible, batch-independent).
+// Every output value is produced by the same operation sequence whatever the
+// stride, so strided grids equal dense[::s, ::s] bit-exactly
+// (tests/test_stats.py:274-285).
+#pragma once
+#include <type_traits>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ssk {
+namespace gk {
+
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u64 pk(float lo, float hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk(u64 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ u64 rcp2(u64 v) {
+  float a, b;
+  upk(v, a, b);
+  return pk(rcp_approx(a), rcp_approx(b));
+}
+__device__ __forceinline__ u64 max0_2(u64 v) {
+  float a, b;
+  upk(v, a, b);
+  return pk(fmaxf(a, 0.f), fmaxf(b, 0.f));
+}
+
+constexpr int G = GS_G;                       // output rows per chunk
+constexpr int VP = GS_VCOLS * 8 + 16;         // V-row pitch (bytes): 8-row reads hit distinct banks
+
+__host__ __device__ constexpr int tw_of(int k) { return ((GS_VCOLS - (k - 1)) / 16) * 16; }
+
+// raw sample (as stored) -> float with the 2^23 splice for small integers
+template <typename TIN>
+__device__ __forceinline__ float raw_to_float(const unsigned char* p) {
+  if constexpr (sizeof(TIN) == 1) {
+    return __int_as_float(0x4B000000 | (unsigned)*p);
+  } else if constexpr (sizeof(TIN) == 2) {
+    return __int_as_float(0x4B000000 | (unsigned)*reinterpret_cast<const unsigned short*>(p));
+  } else if constexpr (std::is_same<TIN, float>::value) {
+    return *reinterpret_cast<const float*>(p);
+  } else {
+    return __uint2float_rn(*reinterpret_cast<const unsigned*>(p));
+  }
+}
+
+template <int K, typename TIN>
+__global__ void __launch_bounds__(GS_THREADS, 4) gauss_pair_kernel(const __grid_constant__ GaussArgs a) {
+  constexpr int TW = tw_of(K);
+  constexpr int TWI = TW + K - 1;
+  constexpr int ES = (int)sizeof(TIN);
+  constexpr int RB = ((TWI * ES + 15) / 16) * 16;  // raw row bytes per image
+  constexpr int NCH = RB / 16;
+  constexpr int RR = 2 * G + K - 1;                 // raw ring rows
+  constexpr int NH = (K + 1) / 2;
+  constexpr int NP = 8 + K - 1;                     // V values read per H item
+  static_assert(TWI <= GS_THREADS, "strip wider than the CTA");
+
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* raw = smem;                        // [RR][4][RB]
+  unsigned char* vbuf = smem + RR * 4 * RB;         // [5][G][VP]
+  __shared__ float s_taps[32];
+  __shared__ double s_red[(GS_THREADS / 32) * 6];
+
+  const int tid = threadIdx.x;
+  const int strip = blockIdx.x, seg = blockIdx.y;
+  const int f0 = 2 * blockIdx.z;
+  const bool has1 = f0 + 1 < a.n;
+  const int f1 = has1 ? f0 + 1 : f0;
+  const int c0 = strip * TW;
+  const int y0 = seg * a.seg_rows;
+  const int y1 = min(y0 + a.seg_rows, a.ho);
+  const int in_end = y1 + K - 1;
+  const int nchunks = (y1 - y0 + G - 1) / G;
+
+  // staged images: 0 = ref f0, 1 = ref f1, 2 = dist f0, 3 = dist f1
+  const long long fo0 = (long long)f0 * a.frame_pitch_b, fo1 = (long long)f1 * a.frame_pitch_b;
+  const int row_bytes_left = (a.w - c0) * ES;
+
+  auto stage_rows = [&](int r_lo, int r_hi) {
+    r_hi = min(r_hi, in_end);
+    const int total = (r_hi - r_lo) * 4 * NCH;
+    for (int i = tid; i < total; i += GS_THREADS) {
+      const int rr = i / (4 * NCH);
+      const int rem = i - rr * (4 * NCH);
+      const int im = rem / NCH;
+      const int q = rem - im * NCH;
+      const int row = r_lo + rr;
+      const int off = q * 16;
+      int valid = row_bytes_left - off;
+      valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
+      const unsigned char* rowp =
+          ((im & 2) ? a.dist : a.ref) + ((im & 1) ? fo1 : fo0) + (long long)row * a.row_pitch_b;
+      const unsigned char* src = valid ? rowp + (long long)c0 * ES + off : rowp;
+      const int slot = (row - y0) % RR;
+      cp_async16(raw + (slot * 4 + im) * RB + off, src, valid);
+    }
+    cp_async_commit();
+  };
+
+  stage_rows(y0, y0 + G + K - 1);
+  if (tid < 32) s_taps[tid] = a.taps[tid];
+  __syncthreads();
+  u64 w2[NH];
+#pragma unroll
+  for (int i = 0; i < NH; ++i) w2[i] = pk(s_taps[i], s_taps[i]);
+
+  const u64 scale2 = pk(a.conv_scale, a.conv_scale);
+  const u64 bias2 = pk(a.conv_bias, a.conv_bias);
+  const u64 shift2 = pk(a.shift, a.shift);
+  const u64 c1_2 = pk(a.c1, a.c1), c2_2 = pk(a.c2, a.c2);
+  const u64 two2 = pk(2.f, 2.f), half2 = pk(0.5f, 0.5f);
+  const bool full_terms = (a.want & (SSK_WANT_Q | SSK_WANT_L)) != 0;
+  const bool want_maps = (a.want & (SSK_MAP_TERMS | SSK_MAP_STATS)) != 0;
+  const int s = a.stride;
+
+  double tq0 = 0.0, tl0 = 0.0, tc0 = 0.0, tq1 = 0.0, tl1 = 0.0, tc1 = 0.0;
+  const int hg = tid & 7, hj = tid >> 3;  // H item: output row hg of the chunk, columns 8*hj..8*hj+7
+
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) {
+      stage_rows(y0 + (c + 1) * G + K - 1, y0 + (c + 2) * G + K - 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+
+    // ---------------- V pass: thread = input column ----------------
+    if (tid < TWI) {
+      u64 acc[5][G];
+#pragma unroll
+      for (int m = 0; m < 5; ++m)
+#pragma unroll
+        for (int r = 0; r < G; ++r) acc[m][r] = 0ull;
+      const int s0 = (c * G) % RR;
+#pragma unroll
+      for (int u = 0; u < G + K - 1; ++u) {
+        int slot = s0 + u;
+        slot = slot >= RR ? slot - RR : slot;
+        const unsigned char* rp = raw + slot * 4 * RB + tid * ES;
+        const u64 X = fma2(pk(raw_to_float<TIN>(rp), raw_to_float<TIN>(rp + RB)), scale2, bias2);
+        const u64 Y = fma2(pk(raw_to_float<TIN>(rp + 2 * RB), raw_to_float<TIN>(rp + 3 * RB)), scale2, bias2);
+        const u64 P[5] = {X, Y, mul2(X, X), mul2(Y, Y), mul2(X, Y)};
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+          const int i = u - r;
+          if (i >= 0 && i < K) {
+            const u64 wi = w2[i < K - 1 - i ? i : K - 1 - i];
+#pragma unroll
+            for (int m = 0; m < 5; ++m) acc[m][r] = fma2(wi, P[m], acc[m][r]);
+          }
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 5; ++m)
+#pragma unroll
+        for (int r = 0; r < G; ++r)
+          *reinterpret_cast<u64*>(vbuf + (m * G + r) * VP + tid * 8) = acc[m][r];
+    }
+    __syncthreads();
+
+    // ---------------- H pass + epilogue: thread = (row, 8 columns) ----------------
+    const int orow = y0 + c * G + hg;
+    if (8 * hj < TW && orow < y1 && (s == 1 || orow % s == 0)) {
+      u64 acc[5][8];
+#pragma unroll
+      for (int m = 0; m < 5; ++m) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) acc[m][jj] = 0ull;
+        const uint4* vr = reinterpret_cast<const uint4*>(vbuf + (m * G + hg) * VP + hj * 64);
+#pragma unroll
+        for (int p2 = 0; p2 < (NP + 1) / 2; ++p2) {
+          const uint4 v4 = vr[p2];
+          const u64 v[2] = {((u64)v4.y << 32) | v4.x, ((u64)v4.w << 32) | v4.z};
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int p = 2 * p2 + h;
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const int i = p - jj;
+              if (i >= 0 && i < K) acc[m][jj] = fma2(w2[i < K - 1 - i ? i : K - 1 - i], v[h], acc[m][jj]);
+            }
+          }
+        }
+      }
+      u64 sq = 0ull, sl = 0ull, scs = 0ull;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int col = c0 + 8 * hj + jj;
+        if (8 * hj + jj < TW && col < a.wo && (s == 1 || col % s == 0)) {
+          const u64 m1 = acc[0][jj], m2 = acc[1][jj];
+          const u64 v1 = max0_2(sub2(acc[2][jj], mul2(m1, m1)));
+          const u64 v2 = max0_2(sub2(acc[3][jj], mul2(m2, m2)));
+          const u64 cv = sub2(acc[4][jj], mul2(m1, m2));
+          const u64 num2 = fma2(two2, cv, c2_2);
+          const u64 den2 = add2(add2(v1, v2), c2_2);
+          const u64 cs = mul2(num2, rcp2(den2));
+          u64 l = 0ull, q = cs;
+          const u64 mu1 = add2(m1, shift2), mu2 = add2(m2, shift2);
+          if (full_terms) {
+            const u64 num1 = fma2(add2(mu1, mu1), mu2, c1_2);
+            // mu1^2 + mu2^2 as ((mu1+mu2)^2 + (mu1-mu2)^2) / 2: exactly symmetric in (ref, dist)
+            const u64 sm = add2(mu1, mu2), df = sub2(mu1, mu2);
+            const u64 den1 = fma2(half2, fma2(df, df, mul2(sm, sm)), c1_2);
+            l = mul2(num1, rcp2(den1));
+            q = mul2(l, cs);
+            sq = add2(sq, q);
+            sl = add2(sl, l);
+          }
+          scs = add2(scs, cs);
+          if (want_maps) {
+            const long long idx = (long long)(orow / s) * a.gw + (col / s);
+            float lo, hi;
+            float* mp0 = reinterpret_cast<float*>(a.maps) + (long long)f0 * a.map_frame + idx;
+            float* mp1 = reinterpret_cast<float*>(a.maps) + (long long)f1 * a.map_frame + idx;
+            const u64 vals[5] = {a.want & SSK_MAP_TERMS ? l : mu1, a.want & SSK_MAP_TERMS ? cs : mu2,
+                                 a.want & SSK_MAP_TERMS ? q : v1, v2, cv};
+            const int nplanes = (a.want & SSK_MAP_TERMS) ? 3 : 5;
+#pragma unroll
+            for (int pl = 0; pl < 5; ++pl) {
+              if (pl < nplanes) {
+                upk(vals[pl], lo, hi);
+                mp0[pl * a.map_plane] = lo;
+                if (has1) mp1[pl * a.map_plane] = hi;
+              }
+            }
+          }
+        }
+      }
+      float lo, hi;
+      upk(sq, lo, hi);
+      tq0 += lo;
+      tq1 += hi;
+      upk(sl, lo, hi);
+      tl0 += lo;
+      tl1 += hi;
+      upk(scs, lo, hi);
+      tc0 += lo;
+      tc1 += hi;
+    }
+  }
+
+  double v[6] = {tq0, tl0, tc0, tq1, tl1, tc1};
+#pragma unroll
+  for (int i = 0; i < 6; ++i) v[i] = warp_sum(v[i]);
+  if ((tid & 31) == 0) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) s_red[(tid >> 5) * 6 + i] = v[i];
+  }
+  __syncthreads();
+  if (tid < 6 && (tid < 3 || has1)) {
+    double t = 0.0;
+#pragma unroll
+    for (int wi = 0; wi < GS_THREADS / 32; ++wi) t += s_red[wi * 6 + tid];
+    const int fr = tid < 3 ? f0 : f1;
+    const long long part = ((long long)fr * gridDim.y + seg) * gridDim.x + strip;
+    a.partials[part * 3 + (tid % 3)] = t;
+  }
+}
+
+template <int K, typename TIN>
+inline size_t smem_bytes() {
+  constexpr int TWI = tw_of(K) + K - 1;
+  constexpr int RB = ((TWI * (int)sizeof(TIN) + 15) / 16) * 16;
+  return (size_t)(2 * G + K - 1) * 4 * RB + (size_t)5 * G * VP;
+}
+
+template <int K, typename TIN>
+int launch_one(const GaussArgs& a, dim3 grid, cudaStream_t st) {
+  auto fn = gauss_pair_kernel<K, TIN>;
+  const size_t smem = smem_bytes<K, TIN>();
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SSK_E_CUDA;
+  fn<<<grid, GS_THREADS, smem, st>>>(a);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+}
+
+template <typename TIN>
+int launch_dtype(const GaussArgs& a, dim3 grid, int k, cudaStream_t st) {
+  switch (k) {
+    case 3: return launch_one<3, TIN>(a, grid, st);
+    case 5: return launch_one<5, TIN>(a, grid, st);
+    case 7: return launch_one<7, TIN>(a, grid, st);
+    case 9: return launch_one<9, TIN>(a, grid, st);
+    case 11: return launch_one<11, TIN>(a, grid, st);
+    case 13: return launch_one<13, TIN>(a, grid, st);
+    case 15: return launch_one<15, TIN>(a, grid, st);
+    case 17: return launch_one<17, TIN>(a, grid, st);
+    case 19: return launch_one<19, TIN>(a, grid, st);
+    case 21: return launch_one<21, TIN>(a, grid, st);
+    case 23: return launch_one<23, TIN>(a, grid, st);
+    case 25: return launch_one<25, TIN>(a, grid, st);
+    case 27: return launch_one<27, TIN>(a, grid, st);
+    case 29: return launch_one<29, TIN>(a, grid, st);
+    case 31: return launch_one<31, TIN>(a, grid, st);
+    default: return SSK_E_SHAPE;
+  }
+}
+
+}  // namespace gk
+}  // namespace ssk

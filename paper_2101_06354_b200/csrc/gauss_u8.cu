@@ -1,0 +1,8 @@
+// Instantiations of the fused Gaussian SSIM kernel for u8 samples (see gauss_ssim.cuh).
+#include "gauss_ssim.cuh"
+
+namespace ssk {
+int launch_gauss_u8(const GaussArgs& a, dim3 grid, int k, cudaStream_t st) {
+  return gk::launch_dtype<uint8_t>(a, grid, k, st);
+}
+}  // namespace ssk

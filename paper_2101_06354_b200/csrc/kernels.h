@@ -6,10 +6,9 @@
 namespace ssk {
 
 // ---------------- K1: Gaussian window ----------------
-constexpr int GS_THREADS = 128;  // one output column per thread in the V pass
-constexpr int GS_TW = 128;       // output columns per strip
-constexpr int GS_G = 8;          // input rows per chunk
-constexpr int GS_HP = 132;       // ring row pitch in floats (== 4 mod 32: conflict-free float4 rows)
+constexpr int GS_THREADS = 128;  // one input column per thread in the V pass
+constexpr int GS_VCOLS = 128;    // input columns per strip (output columns: 16-aligned 128 - (k - 1))
+constexpr int GS_G = 8;          // output rows per chunk
 
 struct GaussArgs {
   const unsigned char* ref;
@@ -20,20 +19,22 @@ struct GaussArgs {
   int ho, wo;                 // dense output extents (h-k+1, w-k+1)
   int gh, gw, stride;         // anchor grid
   int seg_rows;               // output rows per segment (gridDim.y segments)
-  int in_pitch;               // staging row pitch, bytes
   float conv_scale, conv_bias;  // shifted sample = fma(raw_or_biased, scale, bias)
   float shift;                // added back to the means
   float c1, c2;
   int want;
   float taps[32];
-  double* partials;           // [n][gridDim.y][gridDim.x][3]
+  double* partials;           // [n][gridDim.y][gridDim.x][3]; gridDim.z = ceil(n / 2) frame pairs
   void* maps;                 // float32 [n][planes][gh][gw]
   long long map_plane, map_frame;
 };
 
-int gauss_in_pitch(int k, int esize);
-size_t gauss_smem_bytes(int k, int in_pitch);
+inline int gauss_tw(int k) { return ((GS_VCOLS - (k - 1)) / 16) * 16; }  // output columns per strip
 int launch_gauss(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
+int launch_gauss_u8(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
+int launch_gauss_u16(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
+int launch_gauss_u32(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
+int launch_gauss_f32(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 
 // ---------------- K2: rect window ----------------
 constexpr int BX_THREADS = 128;  // one input column per thread in the V pass
@@ -66,7 +67,7 @@ int launch_box_int(const BoxArgs& a, dim3 grid, bool wide, cudaStream_t st);
 int launch_box_float(const BoxArgs& a, dim3 grid, dim3 block, cudaStream_t st);
 
 // ---------------- helpers ----------------
-int launch_reduce_partials(const double* partials, int nparts, int n, int ncomp, double mul,
+int launch_reduce_partials(const double* partials, int nparts, int n, int ncomp, double divisor,
                            double* out, int out_stride, int out_offset, int comp_offset,
                            cudaStream_t st);
 int launch_downsample(const unsigned char* src_r, const unsigned char* src_d, int src_dtype,

@@ -254,5 +254,13 @@ def to_float64(pair_tensor, code: int, scale_log2: int):
     return v * (2.0 ** -scale_log2) if scale_log2 else v
 
 
+def frame_means(sums, count: int):
+    """sums / count with an IEEE division on the device (a 0-dim CUDA divisor, so torch
+    does not substitute a reciprocal multiply); every path derives means this way,
+    so per-pair and batched scores are bit-identical."""
+    torch = nat.torch_mod()
+    return sums / torch.full((), float(count), dtype=torch.float64, device=sums.device)
+
+
 def launch_count() -> int:
     return int(nat.lib().ssk_launch_count())

@@ -83,7 +83,7 @@ def ssim_terms(ref: PlaneLike, dist: PlaneLike, config: SsimConfig = SsimConfig(
     pair, (h, w) = _prepare(ref, dist, config)
     sums, _ = engine.ssim(pair, config.window, config.c1, config.c2, nat.WANT_Q | nat.WANT_L | nat.WANT_CS)
     gh, gw = engine.grid_shape(h, w, config.window.k, config.window.stride)
-    s = sums[0].cpu().numpy() / float(gh * gw)
+    s = engine.frame_means(sums, gh * gw)[0].cpu().numpy()
     return float(s[0]), float(s[1]), float(s[2])
 
 
