@@ -47,24 +47,60 @@ int launch_reduce_partials(const double* partials, int nparts, int n, int ncomp,
 // exactly like the reference's numpy expression.
 // ---------------------------------------------------------------------------
 template <typename TS, typename TD>
-__global__ void downsample_kernel(const unsigned char* __restrict__ src_r,
-                                  const unsigned char* __restrict__ src_d, long long src_rp,
-                                  long long src_fp, int h2, int w2, unsigned char* __restrict__ dst_r,
-                                  unsigned char* __restrict__ dst_d, long long dst_rp,
-                                  long long dst_fp) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(128) downsample_kernel(const unsigned char* __restrict__ src_r,
+                                                         const unsigned char* __restrict__ src_d, long long src_rp,
+                                                         long long src_fp, int h2, int w2,
+                                                         unsigned char* __restrict__ dst_r,
+                                                         unsigned char* __restrict__ dst_d, long long dst_rp,
+                                                         long long dst_fp) {
+  // thread -> 8 adjacent outputs of one row: 16 input samples from each of two rows,
+  // read as whole 16-byte vectors (row pitches are 16-byte multiples by contract)
+  const int x8 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   const int y = blockIdx.y;
   const int f = blockIdx.z >> 1;
   const int img = blockIdx.z & 1;
-  if (x >= w2) return;
+  if (x8 >= w2) return;
   const TS* s = reinterpret_cast<const TS*>((img ? src_d : src_r)) + f * src_fp;
-  TD* d = reinterpret_cast<TD*>((img ? dst_d : dst_r)) + f * dst_fp;
-  const TS* r0 = s + (long long)(2 * y) * src_rp + 2 * x;
+  TD* d = reinterpret_cast<TD*>((img ? dst_d : dst_r)) + f * dst_fp + (long long)y * dst_rp + x8;
+  const TS* r0 = s + (long long)(2 * y) * src_rp + 2 * x8;
   const TS* r1 = r0 + src_rp;
-  if constexpr (std::is_floating_point<TS>::value) {
-    d[(long long)y * dst_rp + x] = (TD)((((r0[0] + r0[1]) + r1[0]) + r1[1]) / (TS)4);
+  constexpr int NV = 16 * (int)sizeof(TS) / 16;  // 16-byte vectors per 16 samples
+  TS a0[16], a1[16];
+  if (x8 + 8 <= w2) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      reinterpret_cast<uint4*>(a0)[i] = reinterpret_cast<const uint4*>(r0)[i];
+      reinterpret_cast<uint4*>(a1)[i] = reinterpret_cast<const uint4*>(r1)[i];
+    }
   } else {
-    d[(long long)y * dst_rp + x] = (TD)((uint32_t)r0[0] + r0[1] + r1[0] + r1[1]);
+    const int n = 2 * (w2 - x8);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      a0[i] = i < n ? r0[i] : (TS)0;
+      a1[i] = i < n ? r1[i] : (TS)0;
+    }
+  }
+  TD o[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if constexpr (std::is_floating_point<TS>::value) {
+      o[i] = (TD)((((a0[2 * i] + a0[2 * i + 1]) + a1[2 * i]) + a1[2 * i + 1]) / (TS)4);
+    } else {
+      o[i] = (TD)((uint32_t)a0[2 * i] + a0[2 * i + 1] + a1[2 * i] + a1[2 * i + 1]);
+    }
+  }
+  if (x8 + 8 <= w2 && ((reinterpret_cast<uintptr_t>(d) & 15) == 0)) {
+    constexpr int NO = 8 * (int)sizeof(TD) / 16 > 0 ? 8 * (int)sizeof(TD) / 16 : 1;
+    if constexpr (8 * sizeof(TD) >= 16) {
+#pragma unroll
+      for (int i = 0; i < NO; ++i) reinterpret_cast<uint4*>(d)[i] = reinterpret_cast<const uint4*>(o)[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) d[i] = o[i];
+    }
+  } else {
+    const int n = min(8, w2 - x8);
+    for (int i = 0; i < n; ++i) d[i] = o[i];
   }
 }
 
@@ -73,7 +109,7 @@ static void ds_launch(const unsigned char* sr, const unsigned char* sd, long lon
                       int n, int h2, int w2, unsigned char* dr, unsigned char* dd, long long drp,
                       long long dfp, cudaStream_t st) {
   dim3 block(128);
-  dim3 grid((w2 + 127) / 128, h2, 2 * n);
+  dim3 grid((w2 + 8 * 128 - 1) / (8 * 128), h2, 2 * n);
   downsample_kernel<TS, TD><<<grid, block, 0, st>>>(sr, sd, srp, sfp, h2, w2, dr, dd, drp, dfp);
 }
 

@@ -305,6 +305,12 @@ int ssk_downsample(const ssk_planes* src, void* d_dst_ref, void* d_dst_dist, int
   if (!src || !src->ref || !src->dist || !d_dst_ref || !d_dst_dist) return SSK_E_ARG;
   if (esize_of(src->dtype) == 0 || esize_of(dst_dtype) == 0 || src->n < 1) return SSK_E_ARG;
   if (src->h < 2 || src->w < 2) return SSK_E_TOO_SMALL;
+  const int es = esize_of(src->dtype), ed = esize_of(dst_dtype);
+  if ((reinterpret_cast<uintptr_t>(src->ref) & 15) || (reinterpret_cast<uintptr_t>(src->dist) & 15) ||
+      ((src->row_pitch * es) & 15) || ((src->frame_pitch * es) & 15) ||
+      (reinterpret_cast<uintptr_t>(d_dst_ref) & 15) || (reinterpret_cast<uintptr_t>(d_dst_dist) & 15) ||
+      ((dst_row_pitch * ed) & 15) || ((dst_frame_pitch * ed) & 15))
+    return SSK_E_ALIGN;
   return launch_downsample(static_cast<const unsigned char*>(src->ref),
                            static_cast<const unsigned char*>(src->dist), src->dtype, src->row_pitch,
                            src->frame_pitch, src->n, src->h, src->w,

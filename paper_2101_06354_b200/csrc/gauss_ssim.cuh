@@ -88,7 +88,7 @@ __device__ __forceinline__ u64 max0_2(u64 v) {
 }
 
 constexpr int G = GS_G;                       // output rows per chunk
-constexpr int VP = GS_VCOLS * 8 + 16;         // V-row pitch (bytes): 8-row reads hit distinct banks
+constexpr int VP = GS_VCOLS * 8 + 8;          // V-row pitch (bytes): a half warp's 8 rows x 2 column groups hit distinct banks
 
 __host__ __device__ constexpr int tw_of(int k) { return ((GS_VCOLS - (k - 1)) / 16) * 16; }
 
@@ -106,8 +106,22 @@ __device__ __forceinline__ float raw_to_float(const unsigned char* p) {
   }
 }
 
-template <int K, typename TIN>
-__global__ void __launch_bounds__(GS_THREADS, 4) gauss_pair_kernel(const __grid_constant__ GaussArgs a) {
+// symmetric (ref <-> dist) a*a + b*b per lane: IEEE-rounded products and sum, never contracted
+__device__ __forceinline__ u64 sumsq2(u64 x, u64 y) {
+  float x0, x1, y0, y1;
+  upk(x, x0, x1);
+  upk(y, y0, y1);
+  return pk(__fadd_rn(__fmul_rn(x0, x0), __fmul_rn(y0, y0)), __fadd_rn(__fmul_rn(x1, x1), __fmul_rn(y1, y1)));
+}
+
+// NM = 4 moments (x, y, x^2+y^2, xy) for the score/term path: sigma1^2 + sigma2^2
+// only enters SSIM as a sum, so one filtered moment fewer (-20% filter FMAs);
+// the variance clamp max(., 0) of stats_from_sums (src/stats.py:199-200) is then
+// applied to the sum (differs from per-variance clamping only by fp32 rounding
+// residue of flat windows).  NM = 5 (x, y, x^2, y^2, xy) serves the statistics
+// maps of local_statistics.
+template <int K, typename TIN, int NM>
+__global__ void __launch_bounds__(GS_THREADS, NM == 4 ? 4 : 3) gauss_pair_kernel(const __grid_constant__ GaussArgs a) {
   constexpr int TW = tw_of(K);
   constexpr int TWI = TW + K - 1;
   constexpr int ES = (int)sizeof(TIN);
@@ -120,7 +134,7 @@ __global__ void __launch_bounds__(GS_THREADS, 4) gauss_pair_kernel(const __grid_
 
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* raw = smem;                        // [RR][4][RB]
-  unsigned char* vbuf = smem + RR * 4 * RB;         // [5][G][VP]
+  unsigned char* vbuf = smem + RR * 4 * RB;         // [NM][G][VP]
   __shared__ float s_taps[32];
   __shared__ double s_red[(GS_THREADS / 32) * 6];
 
@@ -175,6 +189,7 @@ __global__ void __launch_bounds__(GS_THREADS, 4) gauss_pair_kernel(const __grid_
   const bool full_terms = (a.want & (SSK_WANT_Q | SSK_WANT_L)) != 0;
   const bool want_maps = (a.want & (SSK_MAP_TERMS | SSK_MAP_STATS)) != 0;
   const int s = a.stride;
+  const int wo = a.wo;
 
   double tq0 = 0.0, tl0 = 0.0, tc0 = 0.0, tq1 = 0.0, tl1 = 0.0, tc1 = 0.0;
   const int hg = tid & 7, hj = tid >> 3;  // H item: output row hg of the chunk, columns 8*hj..8*hj+7
@@ -189,10 +204,10 @@ __global__ void __launch_bounds__(GS_THREADS, 4) gauss_pair_kernel(const __grid_
     __syncthreads();
 
     // ---------------- V pass: thread = input column ----------------
-    if (tid < TWI) {
-      u64 acc[5][G];
+    if (tid < TWI && c0 + tid < a.w) {
+      u64 acc[NM][G];
 #pragma unroll
-      for (int m = 0; m < 5; ++m)
+      for (int m = 0; m < NM; ++m)
 #pragma unroll
         for (int r = 0; r < G; ++r) acc[m][r] = 0ull;
       const int s0 = (c * G) % RR;
@@ -203,19 +218,29 @@ __global__ void __launch_bounds__(GS_THREADS, 4) gauss_pair_kernel(const __grid_
         const unsigned char* rp = raw + slot * 4 * RB + tid * ES;
         const u64 X = fma2(pk(raw_to_float<TIN>(rp), raw_to_float<TIN>(rp + RB)), scale2, bias2);
         const u64 Y = fma2(pk(raw_to_float<TIN>(rp + 2 * RB), raw_to_float<TIN>(rp + 3 * RB)), scale2, bias2);
-        const u64 P[5] = {X, Y, mul2(X, X), mul2(Y, Y), mul2(X, Y)};
+        u64 P[NM];
+        P[0] = X;
+        P[1] = Y;
+        if constexpr (NM == 4) {
+          P[2] = sumsq2(X, Y);
+          P[3] = mul2(X, Y);
+        } else {
+          P[2] = mul2(X, X);
+          P[3] = mul2(Y, Y);
+          P[NM - 1] = mul2(X, Y);
+        }
 #pragma unroll
         for (int r = 0; r < G; ++r) {
           const int i = u - r;
           if (i >= 0 && i < K) {
             const u64 wi = w2[i < K - 1 - i ? i : K - 1 - i];
 #pragma unroll
-            for (int m = 0; m < 5; ++m) acc[m][r] = fma2(wi, P[m], acc[m][r]);
+            for (int m = 0; m < NM; ++m) acc[m][r] = fma2(wi, P[m], acc[m][r]);
           }
         }
       }
 #pragma unroll
-      for (int m = 0; m < 5; ++m)
+      for (int m = 0; m < NM; ++m)
 #pragma unroll
         for (int r = 0; r < G; ++r)
           *reinterpret_cast<u64*>(vbuf + (m * G + r) * VP + tid * 8) = acc[m][r];
@@ -224,49 +249,57 @@ __global__ void __launch_bounds__(GS_THREADS, 4) gauss_pair_kernel(const __grid_
 
     // ---------------- H pass + epilogue: thread = (row, 8 columns) ----------------
     const int orow = y0 + c * G + hg;
-    if (8 * hj < TW && orow < y1 && (s == 1 || orow % s == 0)) {
-      u64 acc[5][8];
+    const int ocol0 = c0 + 8 * hj;
+    if (8 * hj < TW && ocol0 < wo && orow < y1 && (s == 1 || orow % s == 0)) {
+      u64 acc[NM][8];
 #pragma unroll
-      for (int m = 0; m < 5; ++m) {
+      for (int m = 0; m < NM; ++m) {
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) acc[m][jj] = 0ull;
-        const uint4* vr = reinterpret_cast<const uint4*>(vbuf + (m * G + hg) * VP + hj * 64);
+        const u64* vr = reinterpret_cast<const u64*>(vbuf + (m * G + hg) * VP + hj * 64);
 #pragma unroll
-        for (int p2 = 0; p2 < (NP + 1) / 2; ++p2) {
-          const uint4 v4 = vr[p2];
-          const u64 v[2] = {((u64)v4.y << 32) | v4.x, ((u64)v4.w << 32) | v4.z};
+        for (int p = 0; p < NP; ++p) {
+          const u64 v = vr[p];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int p = 2 * p2 + h;
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-              const int i = p - jj;
-              if (i >= 0 && i < K) acc[m][jj] = fma2(w2[i < K - 1 - i ? i : K - 1 - i], v[h], acc[m][jj]);
-            }
+          for (int jj = 0; jj < 8; ++jj) {
+            const int i = p - jj;
+            if (i >= 0 && i < K) acc[m][jj] = fma2(w2[i < K - 1 - i ? i : K - 1 - i], v, acc[m][jj]);
           }
         }
       }
+      // columns of this item inside the anchor grid (all 8 for interior items at stride 1)
+      const int ncol = min(8, wo - ocol0);
       u64 sq = 0ull, sl = 0ull, scs = 0ull;
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) {
-        const int col = c0 + 8 * hj + jj;
-        if (8 * hj + jj < TW && col < a.wo && (s == 1 || col % s == 0)) {
-          const u64 m1 = acc[0][jj], m2 = acc[1][jj];
-          const u64 v1 = max0_2(sub2(acc[2][jj], mul2(m1, m1)));
-          const u64 v2 = max0_2(sub2(acc[3][jj], mul2(m2, m2)));
-          const u64 cv = sub2(acc[4][jj], mul2(m1, m2));
-          const u64 num2 = fma2(two2, cv, c2_2);
-          const u64 den2 = add2(add2(v1, v2), c2_2);
-          const u64 cs = mul2(num2, rcp2(den2));
-          u64 l = 0ull, q = cs;
-          const u64 mu1 = add2(m1, shift2), mu2 = add2(m2, shift2);
+        const u64 m1 = acc[0][jj], m2 = acc[1][jj];
+        u64 v1, v2, cv, den2;
+        if constexpr (NM == 4) {
+          // sigma1^2 + sigma2^2 = E[x^2 + y^2] - (m1^2 + m2^2), clamped as a sum
+          v1 = max0_2(sub2(acc[2][jj], sumsq2(m1, m2)));
+          v2 = 0ull;
+          cv = sub2(acc[3][jj], mul2(m1, m2));
+          den2 = add2(v1, c2_2);
+        } else {
+          v1 = max0_2(sub2(acc[2][jj], mul2(m1, m1)));
+          v2 = max0_2(sub2(acc[3][jj], mul2(m2, m2)));
+          cv = sub2(acc[NM - 1][jj], mul2(m1, m2));
+          den2 = add2(add2(v1, v2), c2_2);
+        }
+        const u64 num2 = fma2(two2, cv, c2_2);
+        const u64 cs = mul2(num2, rcp2(den2));
+        u64 l = 0ull, q = cs;
+        const u64 mu1 = add2(m1, shift2), mu2 = add2(m2, shift2);
+        if (full_terms) {
+          const u64 num1 = fma2(add2(mu1, mu1), mu2, c1_2);
+          const u64 den1 = add2(sumsq2(mu1, mu2), c1_2);
+          l = mul2(num1, rcp2(den1));
+          q = mul2(l, cs);
+        }
+        const int col = ocol0 + jj;
+        const bool valid = jj < ncol && (s == 1 || col % s == 0);
+        if (valid) {
           if (full_terms) {
-            const u64 num1 = fma2(add2(mu1, mu1), mu2, c1_2);
-            // mu1^2 + mu2^2 as ((mu1+mu2)^2 + (mu1-mu2)^2) / 2: exactly symmetric in (ref, dist)
-            const u64 sm = add2(mu1, mu2), df = sub2(mu1, mu2);
-            const u64 den1 = fma2(half2, fma2(df, df, mul2(sm, sm)), c1_2);
-            l = mul2(num1, rcp2(den1));
-            q = mul2(l, cs);
             sq = add2(sq, q);
             sl = add2(sl, l);
           }
@@ -276,9 +309,9 @@ __global__ void __launch_bounds__(GS_THREADS, 4) gauss_pair_kernel(const __grid_
             float lo, hi;
             float* mp0 = reinterpret_cast<float*>(a.maps) + (long long)f0 * a.map_frame + idx;
             float* mp1 = reinterpret_cast<float*>(a.maps) + (long long)f1 * a.map_frame + idx;
-            const u64 vals[5] = {a.want & SSK_MAP_TERMS ? l : mu1, a.want & SSK_MAP_TERMS ? cs : mu2,
-                                 a.want & SSK_MAP_TERMS ? q : v1, v2, cv};
-            const int nplanes = (a.want & SSK_MAP_TERMS) ? 3 : 5;
+            const bool terms = (a.want & SSK_MAP_TERMS) != 0;
+            const u64 vals[5] = {terms ? l : mu1, terms ? cs : mu2, terms ? q : v1, v2, cv};
+            const int nplanes = terms ? 3 : 5;
 #pragma unroll
             for (int pl = 0; pl < 5; ++pl) {
               if (pl < nplanes) {
@@ -321,22 +354,28 @@ __global__ void __launch_bounds__(GS_THREADS, 4) gauss_pair_kernel(const __grid_
   }
 }
 
-template <int K, typename TIN>
+template <int K, typename TIN, int NM>
 inline size_t smem_bytes() {
   constexpr int TWI = tw_of(K) + K - 1;
   constexpr int RB = ((TWI * (int)sizeof(TIN) + 15) / 16) * 16;
-  return (size_t)(2 * G + K - 1) * 4 * RB + (size_t)5 * G * VP;
+  return (size_t)(2 * G + K - 1) * 4 * RB + (size_t)NM * G * VP;
 }
 
-template <int K, typename TIN>
-int launch_one(const GaussArgs& a, dim3 grid, cudaStream_t st) {
-  auto fn = gauss_pair_kernel<K, TIN>;
-  const size_t smem = smem_bytes<K, TIN>();
+template <int K, typename TIN, int NM>
+int launch_nm(const GaussArgs& a, dim3 grid, cudaStream_t st) {
+  auto fn = gauss_pair_kernel<K, TIN, NM>;
+  const size_t smem = smem_bytes<K, TIN, NM>();
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SSK_E_CUDA;
   fn<<<grid, GS_THREADS, smem, st>>>(a);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+}
+
+template <int K, typename TIN>
+int launch_one(const GaussArgs& a, dim3 grid, cudaStream_t st) {
+  // the statistics maps need the five separate moments; everything else runs on four
+  return (a.want & SSK_MAP_STATS) ? launch_nm<K, TIN, 5>(a, grid, st) : launch_nm<K, TIN, 4>(a, grid, st);
 }
 
 template <typename TIN>

@@ -284,3 +284,24 @@ def test_video_sequence_yuv420(cuda, oracle):
     for rec, (r, d) in zip(luma.records, pairs):
         assert np.max(np.abs(np.array([rec.score, rec.l_mean, rec.cs_mean]) -
                              np.array(oracle.ssim_terms(r[0], d[0], **win)))) < SCORE_TOL
+
+
+@pytest.mark.parametrize("h,w", [(5, 7), (33, 130), (64, 2000), (17, 1)])
+@pytest.mark.parametrize("kind", ["u8", "u16", "f64"])
+def test_downsample_shapes_and_dtypes(cuda, oracle, rng, h, w, kind):
+    if w < 2:
+        with pytest.raises(TooSmall):
+            P.dyadic_downsample(np.zeros((h, w), dtype=np.uint8))
+        return
+    if kind == "u8":
+        a = rng.integers(0, 256, (h, w)).astype(np.uint8)
+    elif kind == "u16":
+        a = rng.integers(0, 1024, (h, w)).astype(np.uint16)
+    else:
+        a = rng.uniform(0, 255, (h, w))
+    want = oracle.dyadic_downsample(a)
+    got = P.dyadic_downsample(a)
+    assert got.shape == want.shape and np.array_equal(got, want)
+    got2 = P.dyadic_downsample(got) if min(got.shape) >= 2 else None
+    if got2 is not None:
+        assert np.array_equal(got2, oracle.dyadic_downsample(want))
