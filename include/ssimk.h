@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SSK_ABI_VERSION 1
+#define SSK_ABI_VERSION 2
 
 /* sample storage types */
 enum {
@@ -156,15 +156,21 @@ int ssk_downsample(const ssk_planes* src, void* d_dst_ref, void* d_dst_dist, int
                    int64_t dst_row_pitch, int64_t dst_frame_pitch, void* stream);
 
 /*
- * Whole MS-SSIM pyramid for a batch (scale_scores, src/multiscale.py:36-59):
- * d_level_means [n][levels] float64 = mean(cs) for levels < L-1 and
- * mean(l*cs) at the coarsest level.  If d_ssim_sums is non-null, level 0
- * also yields the plain-SSIM sums [n][3] (sum q, sum l, sum cs) of the same
- * pass (scale 0 is shared).  The exponent-weighted combination
- * (combine_scale_scores, :62-74) is done by the caller in float64.
+ * Whole MS-SSIM pyramid for a batch (scale_scores + combine_scale_scores,
+ * src/multiscale.py:36-74).  One pass builds every pyramid level (exact scaled
+ * integers for integer samples), one fused SSIM pass per sample type scores
+ * the levels, and one finalize kernel writes
+ *   d_level_means [n][levels] float64: mean(cs) for levels < L-1, mean(l*cs)
+ *                 at the coarsest level;
+ *   d_scores      [n] (nullable): the combined score, aggregation 1 = product
+ *                 of max(s, 0)^e, 2 = sum of e*s, with `exponents` (host array,
+ *                 `levels` entries, already renormalised for sum/fast4 as
+ *                 MultiscaleSpec.effective_exponents does); aggregation 0 = none;
+ *   d_ssim_sums   [n][3] (nullable): level-0 (sum q, sum l, sum cs) -- the plain
+ *                 SSIM of the same pass (scale 0 is shared).
  */
-int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels,
-               double* d_level_means, double* d_ssim_sums,
+int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, const double* exponents,
+               int aggregation, double* d_level_means, double* d_scores, double* d_ssim_sums,
                void* d_workspace, size_t workspace_bytes, void* stream);
 
 /* Number of kernels this library has launched since load (for bench.py). */

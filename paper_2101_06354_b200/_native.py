@@ -32,7 +32,7 @@ RECT, GAUSS = 1, 2
 WANT_Q, WANT_L, WANT_CS, MAP_TERMS, MAP_STATS = 1, 2, 4, 8, 16
 E_ARG, E_WINDOW, E_SHAPE, E_WORKSPACE, E_ALIGN, E_CUDA, E_LEVELS, E_TOO_SMALL = range(-1, -9, -1)
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 EXPORTED_SYMBOLS = (
     "ssk_abi_version",
@@ -109,7 +109,7 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         lib.ssk_downsample.restype = i32
         lib.ssk_downsample.argtypes = [pP, vp, vp, i32, i64, i64, vp]
         lib.ssk_msssim.restype = i32
-        lib.ssk_msssim.argtypes = [pP, pW, i32, vp, vp, vp, sz, vp]
+        lib.ssk_msssim.argtypes = [pP, pW, i32, ctypes.POINTER(ctypes.c_double), i32, vp, vp, vp, vp, sz, vp]
         lib.ssk_launch_count.restype = ctypes.c_uint64
         lib.ssk_probe_fp32_tflops.restype = i32
         lib.ssk_probe_fp32_tflops.argtypes = [ctypes.c_double, ctypes.POINTER(ctypes.c_double), vp]

@@ -78,9 +78,8 @@ def msssim_batch(ref, dist, config: SsimConfig = SsimConfig(), spec: Optional[Mu
     k = config.window.k
     if min(h, w) // (1 << (spec.levels - 1)) < k:
         raise TooManyLevels(f"a {k}x{k} window does not fit the coarsest of {spec.levels} scales of a {w}x{h} image")
-    means, ssim_sums = engine.msssim_levels(pair, config.window, config.c1, config.c2, spec.levels,
-                                            with_ssim=with_ssim, stream=stream)
-    score = combine_levels(means, spec)
+    _, score, ssim_sums = engine.msssim_levels(pair, config.window, config.c1, config.c2, spec.levels,
+                                               with_ssim=with_ssim, spec=spec, stream=stream)
     if not with_ssim:
         return score
     gh, gw = engine.grid_shape(h, w, k, config.window.stride)

@@ -269,3 +269,184 @@ int probe_fp32(double seconds, double* tflops, cudaStream_t st) {
 }
 
 }  // namespace ssk
+
+namespace ssk {
+
+// ---------------------------------------------------------------------------
+// Whole dyadic pyramid in one pass (src/multiscale.py:19-33 applied level after
+// level).  Thread -> one BxB block (B = 2^NL) of the source plane: it reads the
+// block once (16-byte vector rows) and emits the block's samples of every level
+// 1..NL, each level formed from the previous one exactly as the reference does
+// (integer planes: exact sums of 4, scale 4^-l tracked by the caller; float
+// planes: ((a00+a01)+a10)+a11)/4 per level).  Level dims nest as floor(h/2^l), so
+// every level-l sample lies inside exactly one block.
+// ---------------------------------------------------------------------------
+template <typename TS, typename TD, int NL>
+__global__ void __launch_bounds__(128) pyramid_kernel(const __grid_constant__ PyramidArgs p) {
+  constexpr int B = 1 << NL;
+  constexpr bool FLT = std::is_floating_point<TS>::value;
+  using TA = typename std::conditional<FLT, TS, uint32_t>::type;  // working type
+  const int bx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int by = blockIdx.y;
+  const int f = blockIdx.z >> 1, img = blockIdx.z & 1;
+  if (bx * B >= 2 * p.wl[0]) return;  // no level-1 sample in this block
+  const TS* src = reinterpret_cast<const TS*>(img ? p.src_d : p.src_r) + (long long)f * p.src_fp;
+  const int r0 = by * B, c0 = bx * B;
+  // level-1 rows of the block, kept in registers for the coarser levels
+  TA lv[B / 2][B / 2];
+  const bool full = (r0 + B <= 2 * p.hl[0]) && (c0 + B <= 2 * p.wl[0]);
+#pragma unroll
+  for (int i = 0; i < B / 2; ++i) {
+    TS a0[B], a1[B];
+    const TS* s0 = src + (long long)(r0 + 2 * i) * p.src_rp + c0;
+    const TS* s1 = s0 + p.src_rp;
+    if (full && (B * sizeof(TS)) % 16 == 0) {
+#pragma unroll
+      for (int v = 0; v < (int)(B * sizeof(TS) / 16); ++v) {
+        reinterpret_cast<uint4*>(a0)[v] = reinterpret_cast<const uint4*>(s0)[v];
+        reinterpret_cast<uint4*>(a1)[v] = reinterpret_cast<const uint4*>(s1)[v];
+      }
+    } else {
+      const bool rok = r0 + 2 * i + 1 < 2 * p.hl[0] + 1 && r0 + 2 * i < 2 * p.hl[0];
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const bool ok = rok && c0 + j < 2 * p.wl[0];
+        a0[j] = ok ? s0[j] : (TS)0;
+        a1[j] = ok ? s1[j] : (TS)0;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < B / 2; ++j) {
+      if constexpr (FLT) {
+        lv[i][j] = (((a0[2 * j] + a0[2 * j + 1]) + a1[2 * j]) + a1[2 * j + 1]) / (TS)4;
+      } else {
+        lv[i][j] = (TA)a0[2 * j] + a0[2 * j + 1] + a1[2 * j] + a1[2 * j + 1];
+      }
+    }
+  }
+  // store level 1, then fold in place to the coarser levels
+#pragma unroll
+  for (int l = 1; l <= NL; ++l) {
+    const int n = B >> l;  // samples per side at level l
+    const int rl = by * n, cl = bx * n;
+    TD* d = reinterpret_cast<TD*>(img ? p.dst_d[l - 1] : p.dst_r[l - 1]) + (long long)f * p.dst_fp[l - 1];
+    if (l > 1) {
+#pragma unroll
+      for (int i = 0; i < B / 2; ++i)
+#pragma unroll
+        for (int j = 0; j < B / 2; ++j)
+          if (i < n && j < n) {
+            if constexpr (FLT) {
+              lv[i][j] = (((lv[2 * i][2 * j] + lv[2 * i][2 * j + 1]) + lv[2 * i + 1][2 * j]) + lv[2 * i + 1][2 * j + 1]) / (TS)4;
+            } else {
+              lv[i][j] = lv[2 * i][2 * j] + lv[2 * i][2 * j + 1] + lv[2 * i + 1][2 * j] + lv[2 * i + 1][2 * j + 1];
+            }
+          }
+    }
+    const bool whole = rl + n <= p.hl[l - 1] && cl + n <= p.wl[l - 1];
+#pragma unroll
+    for (int i = 0; i < B / 2; ++i) {
+      if (i < n && rl + i < p.hl[l - 1]) {
+        TD* row = d + (long long)(rl + i) * p.dst_rp[l - 1] + cl;
+        if (whole) {
+          // n samples of this row are contiguous and n*sizeof(TD)-aligned: one vector store
+          __align__(16) TD v[B / 2];
+#pragma unroll
+          for (int j = 0; j < B / 2; ++j) v[j] = (TD)lv[i][j];
+          const int bytes = n * (int)sizeof(TD);
+          if (bytes >= 16) {
+#pragma unroll
+            for (int q = 0; q < (B / 2) * (int)sizeof(TD) / 16; ++q)
+              if (q * 16 < bytes) reinterpret_cast<uint4*>(row)[q] = reinterpret_cast<const uint4*>(v)[q];
+          } else if (bytes == 8) {
+            *reinterpret_cast<uint2*>(row) = *reinterpret_cast<const uint2*>(v);
+          } else if (bytes == 4) {
+            *reinterpret_cast<uint32_t*>(row) = *reinterpret_cast<const uint32_t*>(v);
+          } else {
+#pragma unroll
+            for (int j = 0; j < B / 2; ++j)
+              if (j < n) row[j] = v[j];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < B / 2; ++j)
+            if (j < n && cl + j < p.wl[l - 1]) row[j] = (TD)lv[i][j];
+        }
+      }
+    }
+  }
+}
+
+template <typename TS, typename TD>
+static int pyr_launch(const PyramidArgs& p, int nl, int n, cudaStream_t st) {
+  const int B = 1 << nl;
+  dim3 block(128);
+  dim3 grid(((2 * p.wl[0] + B - 1) / B + 127) / 128, (2 * p.hl[0] + B - 1) / B, 2 * n);
+  switch (nl) {
+    case 1: pyramid_kernel<TS, TD, 1><<<grid, block, 0, st>>>(p); break;
+    case 2: pyramid_kernel<TS, TD, 2><<<grid, block, 0, st>>>(p); break;
+    case 3: pyramid_kernel<TS, TD, 3><<<grid, block, 0, st>>>(p); break;
+    case 4: pyramid_kernel<TS, TD, 4><<<grid, block, 0, st>>>(p); break;
+    default: return SSK_E_ARG;
+  }
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+}
+
+int launch_pyramid(const PyramidArgs& p, int src_dtype, int dst_dtype, int nl, int n, cudaStream_t st) {
+  if (nl < 1 || nl > GS_MAX_LEVELS || 2 * n > 65535) return SSK_E_ARG;
+  if (src_dtype == SSK_U8 && dst_dtype == SSK_U16) return pyr_launch<uint8_t, uint16_t>(p, nl, n, st);
+  if (src_dtype == SSK_U8 && dst_dtype == SSK_U32) return pyr_launch<uint8_t, uint32_t>(p, nl, n, st);
+  if (src_dtype == SSK_U16 && dst_dtype == SSK_U16) return pyr_launch<uint16_t, uint16_t>(p, nl, n, st);
+  if (src_dtype == SSK_U16 && dst_dtype == SSK_U32) return pyr_launch<uint16_t, uint32_t>(p, nl, n, st);
+  if (src_dtype == SSK_U32 && dst_dtype == SSK_U32) return pyr_launch<uint32_t, uint32_t>(p, nl, n, st);
+  if (src_dtype == SSK_F32 && dst_dtype == SSK_F32) return pyr_launch<float, float>(p, nl, n, st);
+  if (src_dtype == SSK_F64 && dst_dtype == SSK_F64) return pyr_launch<double, double>(p, nl, n, st);
+  return SSK_E_ARG;
+}
+
+// ---------------------------------------------------------------------------
+// MS-SSIM finalize: one warp per frame folds every level's partials (fixed
+// order), writes mean(cs) below the coarsest level / mean(l*cs) at it, the
+// optional level-0 SSIM sums, and the exponent-weighted combination
+// (combine_scale_scores, src/multiscale.py:62-74: product of max(s, 0)^e, or
+// the normalised sum).
+// ---------------------------------------------------------------------------
+__global__ void msssim_finalize_kernel(const __grid_constant__ FinalizeArgs a) {
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (f >= a.n) return;
+  double combined = a.aggregation == 2 ? 0.0 : 1.0;
+  for (int l = 0; l < a.levels; ++l) {
+    const double* p = a.partials[l] + (long long)f * a.nparts[l] * 3;
+    const int comp = (l == a.levels - 1) ? 0 : 2;
+    double s = 0.0;
+    for (int i = lane; i < a.nparts[l]; i += 32) s += p[(long long)i * 3 + comp];
+    s = warp_sum(s);
+    const double mean = __ddiv_rn(s, a.count[l]);
+    if (l == 0 && a.ssim_sums) {
+      for (int c = 0; c < 3; ++c) {
+        double t = 0.0;
+        for (int i = lane; i < a.nparts[0]; i += 32) t += p[(long long)i * 3 + c];
+        t = warp_sum(t);
+        if (lane == 0) a.ssim_sums[(long long)f * 3 + c] = t;
+      }
+    }
+    if (lane == 0) {
+      a.level_means[(long long)f * a.levels + l] = mean;
+      if (a.aggregation == 2) combined += a.exps[l] * mean;
+      else combined *= pow(fmax(mean, 0.0), a.exps[l]);
+    }
+  }
+  if (lane == 0 && a.scores && a.aggregation != 0) a.scores[f] = combined;
+}
+
+int launch_msssim_finalize(const FinalizeArgs& a, cudaStream_t st) {
+  const int threads = 256;
+  const int blocks = (a.n * 32 + threads - 1) / threads;
+  msssim_finalize_kernel<<<blocks, threads, 0, st>>>(a);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+}
+
+}  // namespace ssk

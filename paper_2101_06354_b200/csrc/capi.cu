@@ -194,10 +194,12 @@ struct Level {
   size_t offset_r = 0, offset_d = 0;  // workspace offsets (level >= 1)
 };
 
-int level_dtype(const ssk_planes* p, int level) {
+// Sample type of the scaled integer pyramid: one type for every level >= 1 (the one
+// the deepest level needs), so the whole pyramid is produced by one kernel.
+int level_dtype(const ssk_planes* p, int deepest) {
   if (p->dtype == SSK_F32) return SSK_F32;
   if (p->dtype == SSK_F64) return SSK_F64;
-  const double mx = (std::ldexp(1.0, p->bit_depth) - 1.0) * std::ldexp(1.0, p->scale_log2 + 2 * level);
+  const double mx = (std::ldexp(1.0, p->bit_depth) - 1.0) * std::ldexp(1.0, p->scale_log2 + 2 * deepest);
   return mx <= 65535.0 ? SSK_U16 : SSK_U32;
 }
 
@@ -210,7 +212,7 @@ int plan_pyramid(const ssk_planes* p, const ssk_window* win, int levels, Level* 
     q.h = prev.h / 2;
     q.w = prev.w / 2;
     if (q.h < 1 || q.w < 1) return SSK_E_TOO_SMALL;
-    q.dtype = level_dtype(p, l);
+    q.dtype = level_dtype(p, levels - 1);
     if (q.dtype == SSK_U16 || q.dtype == SSK_U32) q.scale_log2 = p->scale_log2 + 2 * l;
     const int es = esize_of(q.dtype);
     q.row_pitch = (int64_t)(align_up((size_t)q.w * es, 16) / es);
@@ -334,11 +336,13 @@ size_t ssk_msssim_workspace_bytes(const ssk_planes* p, const ssk_window* win, in
   return pyr + parts;
 }
 
-int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, double* d_level_means,
-               double* d_ssim_sums, void* d_workspace, size_t workspace_bytes, void* stream) {
+int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, const double* exponents,
+               int aggregation, double* d_level_means, double* d_scores, double* d_ssim_sums,
+               void* d_workspace, size_t workspace_bytes, void* stream) {
   int rc = check_planes(p);
   if (rc) return rc;
   if (!win || !d_level_means || levels < 1 || levels > 16) return SSK_E_ARG;
+  if (aggregation < 0 || aggregation > 2 || (aggregation && !exponents)) return SSK_E_ARG;
   if ((std::min(p->h, p->w) >> (levels - 1)) < win->k) return SSK_E_LEVELS;
   const size_t need = ssk_msssim_workspace_bytes(p, win, levels);
   if (need == 0) return SSK_E_ARG;
@@ -353,40 +357,80 @@ int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, double* d
     lv[l].planes.ref = ws + lv[l].offset_r;
     lv[l].planes.dist = ws + lv[l].offset_d;
   }
-  size_t part_off = pyr;
-  for (int l = 0; l < levels; ++l) {
-    if (l > 0) {
-      const ssk_planes& a = lv[l - 1].planes;
-      const ssk_planes& b = lv[l].planes;
-      rc = launch_downsample(static_cast<const unsigned char*>(a.ref),
-                             static_cast<const unsigned char*>(a.dist), a.dtype, a.row_pitch,
-                             a.frame_pitch, a.n, a.h, a.w,
-                             const_cast<unsigned char*>(static_cast<const unsigned char*>(b.ref)),
-                             const_cast<unsigned char*>(static_cast<const unsigned char*>(b.dist)),
-                             b.dtype, b.row_pitch, b.frame_pitch, st);
-      if (rc) return rc;
+
+  // 1) the pyramid: up to four levels per pass over the previous top level
+  for (int base = 0; base + 1 < levels;) {
+    const int nl = std::min(GS_MAX_LEVELS, levels - 1 - base);
+    const ssk_planes& s = lv[base].planes;
+    PyramidArgs pa{};
+    pa.src_r = static_cast<const unsigned char*>(s.ref);
+    pa.src_d = static_cast<const unsigned char*>(s.dist);
+    pa.src_rp = s.row_pitch;
+    pa.src_fp = s.frame_pitch;
+    for (int i = 0; i < nl; ++i) {
+      const ssk_planes& d = lv[base + 1 + i].planes;
+      pa.dst_r[i] = const_cast<unsigned char*>(static_cast<const unsigned char*>(d.ref));
+      pa.dst_d[i] = const_cast<unsigned char*>(static_cast<const unsigned char*>(d.dist));
+      pa.dst_rp[i] = d.row_pitch;
+      pa.dst_fp[i] = d.frame_pitch;
+      pa.hl[i] = d.h;
+      pa.wl[i] = d.w;
     }
+    rc = launch_pyramid(pa, s.dtype, lv[base + 1].planes.dtype, nl, p->n, st);
+    if (rc) return rc;
+    base += nl;
+  }
+
+  // 2) SSIM per level: level 0 alone (input type), the coarser levels batched
+  FinalizeArgs fa{};
+  fa.levels = levels;
+  fa.n = p->n;
+  fa.aggregation = aggregation;
+  fa.level_means = d_level_means;
+  fa.scores = d_scores;
+  fa.ssim_sums = d_ssim_sums;
+  for (int l = 0; l < levels; ++l) fa.exps[l] = aggregation ? exponents[l] : 0.0;
+  size_t part_off = pyr;
+  Plan plans[16];
+  for (int l = 0; l < levels; ++l) {
     const bool last = l == levels - 1;
     int want = last ? SSK_WANT_Q : SSK_WANT_CS;
     if (l == 0 && d_ssim_sums) want |= SSK_WANT_Q | SSK_WANT_L | SSK_WANT_CS;
-    Plan pl;
-    rc = plan_ssim(&lv[l].planes, win, want, pl);
+    rc = plan_ssim(&lv[l].planes, win, want, plans[l]);
     if (rc) return rc;
-    double* partials = reinterpret_cast<double*>(ws + part_off);
-    part_off += partial_bytes(pl, p->n);
-    rc = run_plan(pl, partials, nullptr, nullptr, st);
-    if (rc) return rc;
-    const double count = (double)pl.gh * (double)pl.gw;
-    rc = launch_reduce_partials(partials, (int)pl.nparts_per_frame, p->n, 1, count,
-                                d_level_means, levels, l, last ? 0 : 2, st);
-    if (rc) return rc;
-    if (l == 0 && d_ssim_sums) {
-      rc = launch_reduce_partials(partials, (int)pl.nparts_per_frame, p->n, 3, 1.0, d_ssim_sums, 3,
-                                  0, 0, st);
-      if (rc) return rc;
+    fa.partials[l] = reinterpret_cast<const double*>(ws + part_off);
+    fa.nparts[l] = (int)plans[l].nparts_per_frame;
+    fa.count[l] = (double)plans[l].gh * (double)plans[l].gw;
+    if (plans[l].gauss) {
+      plans[l].ga.partials = reinterpret_cast<double*>(ws + part_off);
+      plans[l].ga.maps = nullptr;
     }
+    part_off += partial_bytes(plans[l], p->n);
   }
-  return SSK_OK;
+  for (int l = 0; l < levels;) {
+    if (l == 0 || !plans[l].gauss) {
+      rc = run_plan(plans[l], const_cast<double*>(fa.partials[l]), nullptr, nullptr, st);
+      if (rc) return rc;
+      ++l;
+      continue;
+    }
+    GaussLevels gl{};
+    int ctas = 0;
+    while (l < levels && gl.nlev < GS_MAX_LEVELS && plans[l].gauss) {
+      gl.lv[gl.nlev] = plans[l].ga;
+      gl.cta_off[gl.nlev] = ctas;
+      gl.nstrips[gl.nlev] = (int)plans[l].grid.x;
+      gl.nseg[gl.nlev] = (int)plans[l].grid.y;
+      ctas += (int)(plans[l].grid.x * plans[l].grid.y);
+      ++gl.nlev;
+      ++l;
+    }
+    rc = launch_gauss_levels(gl, dim3(ctas, 1, (p->n + 1) / 2), win->k, gl.lv[0].dtype, st);
+    if (rc) return rc;
+  }
+
+  // 3) per-frame means, level-0 SSIM sums and the combined score
+  return launch_msssim_finalize(fa, st);
 }
 
 uint64_t ssk_launch_count(void) { return g_launches.load(); }

@@ -5,4 +5,7 @@ namespace ssk {
 int launch_gauss_f32(const GaussArgs& a, dim3 grid, int k, cudaStream_t st) {
   return gk::launch_dtype<float>(a, grid, k, st);
 }
+int launch_gauss_levels_f32(const GaussLevels& p, dim3 grid, int k, cudaStream_t st) {
+  return gk::launch_levels_dtype<float>(p, grid, k, st);
+}
 }  // namespace ssk

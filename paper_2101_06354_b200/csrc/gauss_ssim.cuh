@@ -121,7 +121,8 @@ __device__ __forceinline__ u64 sumsq2(u64 x, u64 y) {
 // residue of flat windows).  NM = 5 (x, y, x^2, y^2, xy) serves the statistics
 // maps of local_statistics.
 template <int K, typename TIN, int NM>
-__global__ void __launch_bounds__(GS_THREADS, NM == 4 ? 4 : 3) gauss_pair_kernel(const __grid_constant__ GaussArgs a) {
+__device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, const int seg, const int pair,
+                                           const int nstrips, const int nseg) {
   constexpr int TW = tw_of(K);
   constexpr int TWI = TW + K - 1;
   constexpr int ES = (int)sizeof(TIN);
@@ -139,8 +140,7 @@ __global__ void __launch_bounds__(GS_THREADS, NM == 4 ? 4 : 3) gauss_pair_kernel
   __shared__ double s_red[(GS_THREADS / 32) * 6];
 
   const int tid = threadIdx.x;
-  const int strip = blockIdx.x, seg = blockIdx.y;
-  const int f0 = 2 * blockIdx.z;
+  const int f0 = 2 * pair;
   const bool has1 = f0 + 1 < a.n;
   const int f1 = has1 ? f0 + 1 : f0;
   const int c0 = strip * TW;
@@ -349,9 +349,28 @@ __global__ void __launch_bounds__(GS_THREADS, NM == 4 ? 4 : 3) gauss_pair_kernel
 #pragma unroll
     for (int wi = 0; wi < GS_THREADS / 32; ++wi) t += s_red[wi * 6 + tid];
     const int fr = tid < 3 ? f0 : f1;
-    const long long part = ((long long)fr * gridDim.y + seg) * gridDim.x + strip;
+    const long long part = ((long long)fr * nseg + seg) * nstrips + strip;
     a.partials[part * 3 + (tid % 3)] = t;
   }
+}
+
+template <int K, typename TIN, int NM>
+__global__ void __launch_bounds__(GS_THREADS, NM == 4 ? 4 : 3) gauss_pair_kernel(const __grid_constant__ GaussArgs a) {
+  gauss_body<K, TIN, NM>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.x, gridDim.y);
+}
+
+// All pyramid levels of one sample type in one launch: blockIdx.x enumerates the
+// (level, segment, strip) tiles, so the small coarse levels share the GPU with
+// each other instead of each launching a few dozen CTAs.
+template <int K, typename TIN, int NM>
+__global__ void __launch_bounds__(GS_THREADS, NM == 4 ? 4 : 3) gauss_levels_kernel(const __grid_constant__ GaussLevels p) {
+  int lv = 0;
+#pragma unroll
+  for (int i = 1; i < GS_MAX_LEVELS; ++i)
+    if (i < p.nlev && (int)blockIdx.x >= p.cta_off[i]) lv = i;
+  const int local = blockIdx.x - p.cta_off[lv];
+  const int ns = p.nstrips[lv];
+  gauss_body<K, TIN, NM>(p.lv[lv], local % ns, local / ns, blockIdx.z, ns, p.nseg[lv]);
 }
 
 template <int K, typename TIN, int NM>
@@ -376,6 +395,39 @@ template <int K, typename TIN>
 int launch_one(const GaussArgs& a, dim3 grid, cudaStream_t st) {
   // the statistics maps need the five separate moments; everything else runs on four
   return (a.want & SSK_MAP_STATS) ? launch_nm<K, TIN, 5>(a, grid, st) : launch_nm<K, TIN, 4>(a, grid, st);
+}
+
+template <int K, typename TIN>
+int launch_levels_one(const GaussLevels& p, dim3 grid, cudaStream_t st) {
+  auto fn = gauss_levels_kernel<K, TIN, 4>;
+  const size_t smem = smem_bytes<K, TIN, 4>();
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SSK_E_CUDA;
+  fn<<<grid, GS_THREADS, smem, st>>>(p);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+}
+
+template <typename TIN>
+int launch_levels_dtype(const GaussLevels& p, dim3 grid, int k, cudaStream_t st) {
+  switch (k) {
+    case 3: return launch_levels_one<3, TIN>(p, grid, st);
+    case 5: return launch_levels_one<5, TIN>(p, grid, st);
+    case 7: return launch_levels_one<7, TIN>(p, grid, st);
+    case 9: return launch_levels_one<9, TIN>(p, grid, st);
+    case 11: return launch_levels_one<11, TIN>(p, grid, st);
+    case 13: return launch_levels_one<13, TIN>(p, grid, st);
+    case 15: return launch_levels_one<15, TIN>(p, grid, st);
+    case 17: return launch_levels_one<17, TIN>(p, grid, st);
+    case 19: return launch_levels_one<19, TIN>(p, grid, st);
+    case 21: return launch_levels_one<21, TIN>(p, grid, st);
+    case 23: return launch_levels_one<23, TIN>(p, grid, st);
+    case 25: return launch_levels_one<25, TIN>(p, grid, st);
+    case 27: return launch_levels_one<27, TIN>(p, grid, st);
+    case 29: return launch_levels_one<29, TIN>(p, grid, st);
+    case 31: return launch_levels_one<31, TIN>(p, grid, st);
+    default: return SSK_E_SHAPE;
+  }
 }
 
 template <typename TIN>

@@ -29,6 +29,19 @@ struct GaussArgs {
   long long map_plane, map_frame;
 };
 
+constexpr int GS_MAX_LEVELS = 4;  // pyramid levels fused into one multi-level launch
+
+// Several pyramid levels (same sample type) scored by one launch.
+struct GaussLevels {
+  GaussArgs lv[GS_MAX_LEVELS];
+  int nlev;
+  int cta_off[GS_MAX_LEVELS];  // first blockIdx.x of each level
+  int nstrips[GS_MAX_LEVELS];
+  int nseg[GS_MAX_LEVELS];
+};
+
+int launch_gauss_levels(const GaussLevels& p, dim3 grid, int k, int dtype, cudaStream_t st);
+
 inline int gauss_tw(int k) { return ((GS_VCOLS - (k - 1)) / 16) * 16; }  // output columns per strip
 int launch_gauss(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 int launch_gauss_u8(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
@@ -65,6 +78,32 @@ struct BoxArgs {
 size_t box_smem_bytes(const BoxArgs& a, bool wide);
 int launch_box_int(const BoxArgs& a, dim3 grid, bool wide, cudaStream_t st);
 int launch_box_float(const BoxArgs& a, dim3 grid, dim3 block, cudaStream_t st);
+
+// ---------------- pyramid + MS-SSIM finalize ----------------
+struct PyramidArgs {
+  const unsigned char* src_r;
+  const unsigned char* src_d;
+  long long src_rp, src_fp;                      // elements
+  unsigned char* dst_r[GS_MAX_LEVELS];
+  unsigned char* dst_d[GS_MAX_LEVELS];
+  long long dst_rp[GS_MAX_LEVELS], dst_fp[GS_MAX_LEVELS];
+  int hl[GS_MAX_LEVELS], wl[GS_MAX_LEVELS];       // dims of the produced levels 1..nl
+};
+int launch_pyramid(const PyramidArgs& p, int src_dtype, int dst_dtype, int nl, int n, cudaStream_t st);
+
+constexpr int SSK_MAX_SCALES = 16;
+struct FinalizeArgs {
+  const double* partials[SSK_MAX_SCALES];
+  int nparts[SSK_MAX_SCALES];
+  double count[SSK_MAX_SCALES];
+  double exps[SSK_MAX_SCALES];
+  int levels, n;
+  int aggregation;        // 0: level means only, 1: product, 2: sum
+  double* level_means;    // [n][levels]
+  double* scores;         // [n] or null
+  double* ssim_sums;      // [n][3] or null (level-0 sums of q, l, cs)
+};
+int launch_msssim_finalize(const FinalizeArgs& a, cudaStream_t st);
 
 // ---------------- helpers ----------------
 int launch_reduce_partials(const double* partials, int nparts, int n, int ncomp, double divisor,

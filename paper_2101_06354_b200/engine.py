@@ -177,8 +177,12 @@ def ssim(pair: DevicePair, window, c1: float, c2: float, want: int, stream=None)
 
 
 def msssim_levels(pair: DevicePair, window, c1: float, c2: float, levels: int,
-                  with_ssim: bool = False, stream=None):
-    """Per-level means [n, levels] (cs below the coarsest, q at it) and optional level-0 SSIM sums."""
+                  with_ssim: bool = False, spec=None, stream=None):
+    """Whole MS-SSIM pyramid in one library call.
+
+    Returns (level means [n, levels] (cs below the coarsest, q at it), combined
+    score [n] or None (when ``spec`` is given), level-0 SSIM sums [n, 3] or None).
+    """
     torch = nat.torch_mod()
     lib = nat.lib()
     n, h, w = pair.shape
@@ -187,12 +191,20 @@ def msssim_levels(pair: DevicePair, window, c1: float, c2: float, levels: int,
     dev = pair.ref.device
     means = torch.empty((n, levels), dtype=torch.float64, device=dev)
     ssim_sums = torch.empty((n, 3), dtype=torch.float64, device=dev) if with_ssim else None
+    scores = None
+    exps = None
+    agg = 0
+    if spec is not None:
+        scores = torch.empty((n,), dtype=torch.float64, device=dev)
+        e = spec.effective_exponents()
+        exps = (ctypes.c_double * len(e))(*e)
+        agg = 2 if spec.aggregation == "sum" else 1
     ws_bytes = lib.ssk_msssim_workspace_bytes(ctypes.byref(planes), ctypes.byref(win), levels)
     ws = nat.WORKSPACE.get(max(ws_bytes, 256), dev, stream)
-    rc = lib.ssk_msssim(ctypes.byref(planes), ctypes.byref(win), levels, means.data_ptr(),
-                        _ptr(ssim_sums), ws.data_ptr(), ws.numel(), nat.stream_handle(stream))
+    rc = lib.ssk_msssim(ctypes.byref(planes), ctypes.byref(win), levels, exps, agg, means.data_ptr(),
+                        _ptr(scores), _ptr(ssim_sums), ws.data_ptr(), ws.numel(), nat.stream_handle(stream))
     nat.raise_for(rc, "msssim")
-    return means, ssim_sums
+    return means, scores, ssim_sums
 
 
 def window_sums(pair: DevicePair, k: int, stride: int, stream=None):

@@ -56,7 +56,7 @@ def _level_means(ref: PlaneLike, dist: PlaneLike, config: SsimConfig, levels: in
     resolve_engine(config.window, config.engine)
     bd = plane_bit_depth(ref, config.bit_depth)
     pair = engine.upload_pair(a, b, bd, config.window.shape == "gauss")
-    means, _ = engine.msssim_levels(pair, config.window, config.c1, config.c2, levels)
+    means, _, _ = engine.msssim_levels(pair, config.window, config.c1, config.c2, levels)
     return means[0].cpu().numpy()
 
 

@@ -61,7 +61,8 @@ def test_argument_errors_need_no_gpu():
     win.shape, win.k = nat.RECT, 3
     assert lib.ssk_ssim_workspace_bytes(ctypes.byref(p), ctypes.byref(win)) > 0
     means = ctypes.c_void_p(64)
-    assert lib.ssk_msssim(ctypes.byref(p), ctypes.byref(win), 3, means, None, None, 0, None) == nat.E_LEVELS
+    assert lib.ssk_msssim(ctypes.byref(p), ctypes.byref(win), 3, None, 0, means, None, None, None, 0,
+                          None) == nat.E_LEVELS
 
 
 def test_error_codes_map_to_reference_exceptions():
