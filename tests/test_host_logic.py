@@ -1,0 +1,169 @@
+"""Host-side logic of the drop-in boundary (no GPU): configuration, containers, pooling, errors."""
+
+import numpy as np
+import pytest
+
+import paper_2101_06354_b200 as P
+from paper_2101_06354_b200 import errors as E
+from paper_2101_06354_b200.pooling import parse_spatial, parse_temporal
+
+
+class TestConfig:
+    def test_defaults_match_reference(self):
+        cfg = P.SsimConfig()
+        assert cfg.window == P.WindowSpec.rectangular(11)  # src/config.py:246
+        assert cfg.engine == "auto" and cfg.bit_depth == 8
+        assert cfg.c1 == pytest.approx(6.5025) and cfg.c2 == pytest.approx(58.5225)
+        assert cfg.c3 == cfg.c2 / 2
+        assert P.SsimConfig(bit_depth=10).c1 == pytest.approx(104.6529)
+
+    def test_json_round_trip_bit_exact(self):
+        cfg = P.SsimConfig(k1=0.013, window=P.WindowSpec.gaussian(1.5, stride=2),
+                           multiscale=P.MultiscaleSpec.weighted_sum(3),
+                           color=P.ColorModelSpec("fixed", weights=(0.6, 0.2, 0.2)))
+        assert P.SsimConfig.from_json(cfg.to_json()) == cfg
+
+    def test_window_validation(self):
+        assert P.WindowSpec.gaussian(1.5).k == 11
+        with pytest.raises(E.ValidationError):
+            P.WindowSpec("gauss", 4, 1.0)
+        with pytest.raises(E.NonPositiveSigma):
+            P.WindowSpec.gaussian(0.0, k=3)
+        with pytest.raises(E.ValidationError):
+            P.WindowSpec.rectangular(0)
+        with pytest.raises(E.ValidationError):
+            P.WindowSpec("rect", 5, 1.0)
+        with pytest.raises(E.ValidationError):
+            P.WindowSpec.rectangular(5, stride=0)
+        assert P.WindowSpec.rectangular(8).k == 8  # even rect windows are allowed
+
+    def test_multiscale_spec(self):
+        assert P.MultiscaleSpec.product().exponents == P.STANDARD_EXPONENTS
+        f4 = P.MultiscaleSpec.fast4().effective_exponents()
+        assert sum(f4) == pytest.approx(1.0) and len(f4) == 4
+        with pytest.raises(E.ValidationError):
+            P.MultiscaleSpec("product", 3, (0.5, 0.5))
+        with pytest.raises(E.ValidationError):
+            P.MultiscaleSpec("fast4", 5)
+        with pytest.raises(E.ValidationError):
+            P.MultiscaleSpec.product(6)
+
+    def test_selectors(self):
+        assert P.parse_window("rect:8,stride=4") == P.WindowSpec.rectangular(8, stride=4)
+        assert P.parse_window("gauss:1.5") == P.WindowSpec.gaussian(1.5)
+        assert P.parse_window("gauss:1.5,k=13").k == 13
+        assert P.parse_multiscale("product:levels=3").levels == 3
+        assert P.parse_color("fixed:0.8,0.1,0.1").weights == (0.8, 0.1, 0.1)
+        assert P.parse_color("cw:a=-0.2,b=-0.1").alpha == -0.2
+        for sel in ("rect:11", "gauss:1.5,k=11,stride=2"):
+            assert P.parse_window(sel).selector() == sel
+        with pytest.raises(E.ValidationError):
+            P.parse_window("box:3")
+        with pytest.raises(E.ValidationError):
+            P.SsimConfig(spatial_pool="bogus")
+
+    def test_color_spec_validation(self):
+        with pytest.raises(E.ValidationError):
+            P.ColorModelSpec("fixed", weights=(0.5, 0.2, 0.2))
+        with pytest.raises(E.DegenerateWeights):
+            P.ColorModelSpec("cw", alpha=-0.5, beta=-0.5)
+
+
+class TestContainers:
+    def test_luma_plane_range_and_freeze(self):
+        p = P.LumaPlane(np.array([[0, 255]], dtype=np.uint8))
+        assert not p.samples.flags.writeable
+        with pytest.raises(E.ValidationError):
+            P.LumaPlane(np.array([[0, 256]]))
+        with pytest.raises(E.ValidationError):
+            P.LumaPlane(np.array([[1.0, np.nan]]))
+        with pytest.raises(E.ValidationError):
+            P.LumaPlane(np.zeros((2, 2)), bit_depth=7)
+        assert P.LumaPlane(np.array([[1023]], dtype=np.uint16), 10).peak == 1023.0
+
+    def test_color_frame_420_dims(self):
+        y = np.zeros((5, 7), dtype=np.uint8)
+        c = np.zeros((3, 4), dtype=np.uint8)
+        f = P.ColorFrame((y, c, c), "ycbcr-bt709", "420")
+        assert f.height == 5 and f.width == 7
+        with pytest.raises(E.ValidationError):
+            P.ColorFrame((y, y, y), "ycbcr-bt709", "420")
+
+    def test_quality_map_rejects_non_finite(self):
+        with pytest.raises(E.ValidationError):
+            P.QualityMap(np.array([[np.inf]]))
+        assert P.QualityMap(np.array([[0.5, 1.0]])).mean() == 0.75
+
+    def test_pair_validation(self):
+        a = np.zeros((4, 4), dtype=np.uint8)
+        with pytest.raises(E.DimensionMismatch):
+            P.validate_frame_pair(a, np.zeros((4, 5), dtype=np.uint8))
+        with pytest.raises(E.BitDepthMismatch):
+            P.validate_frame_pair(P.LumaPlane(a, 8), P.LumaPlane(a.astype(np.uint16), 10))
+
+    def test_exception_hierarchy(self):
+        assert issubclass(E.ValidationError, ValueError)
+        for cls in (E.WindowLargerThanImage, E.TooManyLevels, E.EngineShapeMismatch, E.EmptyMap):
+            assert issubclass(cls, P.SsimkitError)
+
+
+class TestPooling:
+    def test_spatial_known_answers(self):
+        # tests/test_pooling.py style known answers
+        v = np.array([[0.25, 0.5], [0.75, 1.0]])
+        assert P.pool_spatial(v, "am") == 0.625
+        assert P.pool_spatial(v, "mink:p=1") == pytest.approx(1 - 0.625)
+        assert P.pool_spatial(v, "pp:ps=6,rs=1") == 0.625
+        assert P.pool_spatial(v, "lw:a=0,b=0", ref_luma=np.ones_like(v)) == 0.625
+        assert P.pool_spatial(v, "md:p=2,o=1") == pytest.approx(float(v.std()))
+        assert P.pool_spatial(np.array([0.1, 0.2, 0.5, 0.8, 0.9]), "fns") == pytest.approx(0.5)
+        with pytest.raises(E.MissingLumaForLW):
+            P.pool_spatial(v, "lw")
+        with pytest.raises(E.EmptyMap):
+            P.pool_spatial(np.zeros((0, 3)), "am")
+
+    def test_temporal(self):
+        s = np.array([0.9, 0.8, 0.7, 0.6])
+        assert P.pool_temporal(s, "am") == pytest.approx(0.75)
+        assert P.pool_temporal(s, "hm") <= P.pool_temporal(s, "gm") <= P.pool_temporal(s, "am")
+        assert P.pool_temporal(s, "median") == pytest.approx(0.75)
+        assert P.pool_temporal(s, "wam:k=2") == pytest.approx(0.75)
+        assert P.pool_temporal(P.ScoreSeries(s), parse_temporal("am")) == pytest.approx(0.75)
+        with pytest.raises(E.EmptySeries):
+            P.pool_temporal(np.array([]), "am")
+        with pytest.raises(E.ZeroMeanCoV):
+            P.pool_temporal(np.array([1.0, -1.0]), "cov")
+
+    def test_selector_round_trip(self):
+        for sel in ("am", "md:p=2,o=3", "lw:a=10,b=5", "pp:ps=6,rs=4"):
+            assert parse_spatial(sel).selector() == sel
+        assert parse_temporal("wam:k=3").selector() == "wam:k=3"
+
+
+def test_gaussian_kernel_host_helper():
+    k = P.gaussian_kernel(1.5)
+    assert k.shape == (11, 11) and abs(k.sum() - 1.0) < 1e-12
+    assert k[5, 5] == pytest.approx(0.07076223776394697, abs=1e-15)
+    assert P.rect_equivalent(1.5, "same-variance") == 7
+    assert P.rect_equivalent(1.5, "same-size") == 11
+
+
+def test_weber_closed_forms():
+    assert P.weber_luminance_term(50.0, 0.1, 0.0) == pytest.approx(0.9954751131221721, abs=1e-15)
+    assert P.weber_luminance_term(50.0, 0.0, 0.3) == 1.0
+    with pytest.raises(ValueError):
+        P.weber_luminance_term(0.0, 0.1, 0.0)
+
+
+def test_no_cpu_fallback():
+    """Scoring without a CUDA device fails loudly instead of computing on the host."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    a = np.zeros((16, 16), dtype=np.uint8)
+    with pytest.raises(E.EngineUnavailable):
+        P.ssim_score(a, a)
+    with pytest.raises(E.EngineUnavailable):
+        P.msssim(np.zeros((64, 64), dtype=np.uint8), np.zeros((64, 64), dtype=np.uint8),
+                 P.SsimConfig(window=P.WindowSpec.rectangular(3)), P.MultiscaleSpec.product(3))
