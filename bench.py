@@ -72,29 +72,52 @@ def generate(indices, workers: int):
 # CPU baseline (oracle port; test infrastructure used only as the measured baseline)
 # ---------------------------------------------------------------------------
 
-def _cpu_pair(i: int) -> float:
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
+def _cpu_score(pair) -> float:
+    """One frame pair through the reference's CPU algorithm (oracle port): ssim_score + msssim."""
     from oracle import ssim_oracle as O
 
-    a, b = _gen(i)
+    a, b = pair
     win = dict(shape="gauss", k=K, sigma=SIGMA)
-    O.ssim_terms(a, b, **win)       # ssim_score path (reference computes it separately)
+    O.ssim_terms(a, b, **win)       # ssim_score path (the reference computes it separately)
     O.msssim(a, b, LEVELS, **win)   # msssim path
     return 1.0
 
 
-def cpu_rate(n_pairs: int, workers: int) -> tuple[float, float]:
-    """(pairs/s, wall seconds) of the oracle on `workers` processes over n_pairs pairs."""
-    from concurrent.futures import ProcessPoolExecutor
+def _cpu_warm(_) -> int:
+    import oracle.ssim_oracle  # noqa: F401  (imports outside the timed region)
 
-    env_keys = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")
-    for k in env_keys:
-        os.environ[k] = "1"
-    t0 = time.perf_counter()
-    with ProcessPoolExecutor(workers) as ex:
-        done = sum(ex.map(_cpu_pair, range(10_000, 10_000 + n_pairs)))
-    wall = time.perf_counter() - t0
-    return done / wall, wall
+    return os.getpid()
+
+
+class CpuBaseline:
+    """A persistent pool of single-threaded worker processes running the oracle port.
+
+    Inputs are generated up front and worker start-up/imports happen before any timing, so the
+    timed region holds only the reference algorithm (plus pickling the 4 MB pair to a worker).
+    """
+
+    def __init__(self, workers: int):
+        from concurrent.futures import ProcessPoolExecutor
+
+        for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[k] = "1"
+        self.workers = workers
+        self.pool = ProcessPoolExecutor(workers)
+        list(self.pool.map(_cpu_warm, range(workers)))
+
+    def rate(self, pairs) -> tuple[float, float]:
+        t0 = time.perf_counter()
+        done = sum(self.pool.map(_cpu_score, pairs))
+        wall = time.perf_counter() - t0
+        return done / wall, wall
+
+    def close(self):
+        self.pool.shutdown()
+
+
+def cpu_pairs(n: int, workers: int):
+    ref, dist = generate(range(10_000, 10_000 + n), workers)
+    return [(ref[i], dist[i]) for i in range(n)]
 
 
 def host_cores() -> int:
@@ -201,12 +224,15 @@ def run_reference(args) -> None:
         return
     cores = host_cores()
     per_step = cores  # one pair per worker process per step
+    pairs = cpu_pairs(per_step, cores)
+    cpu = CpuBaseline(cores)
     for _ in range(args.warmup):
-        cpu_rate(per_step, cores)
+        cpu.rate(pairs)
     t_total = 0.0
     for _ in range(args.steps):
-        _, wall = cpu_rate(per_step, cores)
+        _, wall = cpu.rate(pairs)
         t_total += wall
+    cpu.close()
     value = per_step * args.steps / t_total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -214,8 +240,8 @@ def run_reference(args) -> None:
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": WORKLOAD, "batch": BATCH, "h": H, "w": W, "seed_base": 202},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{per_step} pairs per step (1 per worker process), oracle port of "
-                                   "ssimkit's numpy path (ssim_score + msssim per pair)"},
+                         "sample": f"{per_step} config-2 pairs per step (1 per single-threaded worker process), "
+                                   "oracle port of ssimkit's numpy path (ssim_score + msssim per pair)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -329,10 +355,12 @@ def run_b200(args) -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         n_cpu = cores * args.cpu_pairs_per_core
-        rate, wall = cpu_rate(n_cpu, cores)
+        pool = CpuBaseline(cores)
+        rate, wall = pool.rate(cpu_pairs(n_cpu, cores))
+        pool.close()
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{n_cpu} config-2 pairs ({args.cpu_pairs_per_core} per process), ssim_score + msssim "
-                         f"each, oracle port of ssimkit's numpy algorithms, {wall:.1f} s wall"}
+               "sample": f"{n_cpu} config-2 pairs ({args.cpu_pairs_per_core} per single-threaded process), "
+                         f"ssim_score + msssim each, oracle port of ssimkit's numpy algorithms, {wall:.1f} s wall"}
 
     if rank == 0:
         line = {
@@ -380,7 +408,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-pairs-per-core", type=int, default=1)
+    ap.add_argument("--cpu-pairs-per-core", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
