@@ -185,14 +185,17 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
   const u64 bias2 = pk(a.conv_bias, a.conv_bias);
   const u64 shift2 = pk(a.shift, a.shift);
   const u64 c1_2 = pk(a.c1, a.c1), c2_2 = pk(a.c2, a.c2);
-  const u64 two2 = pk(2.f, 2.f), half2 = pk(0.5f, 0.5f);
+  const u64 two2 = pk(2.f, 2.f);
+  const u64 twoshift2 = pk(2.f * a.shift, 2.f * a.shift);
+  const float c1b = 2.f * a.shift * a.shift + a.c1;  // 2 s^2 + C1 (exact for s = 2^(bd-1))
+  const u64 c1b_2 = pk(c1b, c1b);
   const bool full_terms = (a.want & (SSK_WANT_Q | SSK_WANT_L)) != 0;
   const bool want_maps = (a.want & (SSK_MAP_TERMS | SSK_MAP_STATS)) != 0;
   const int s = a.stride;
   const int wo = a.wo;
 
   double tq0 = 0.0, tl0 = 0.0, tc0 = 0.0, tq1 = 0.0, tl1 = 0.0, tc1 = 0.0;
-  const int hg = tid & 7, hj = tid >> 3;  // H item: output row hg of the chunk, columns 8*hj..8*hj+7
+  const int hg = tid % G, hj = tid / G;  // H item: output row hg of the chunk, columns 8*hj..8*hj+7
 
   for (int c = 0; c < nchunks; ++c) {
     if (c + 1 < nchunks) {
@@ -222,7 +225,10 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
         P[0] = X;
         P[1] = Y;
         if constexpr (NM == 4) {
-          P[2] = sumsq2(X, Y);
+          // x'^2 and y'^2 are exact for 8-bit samples (|x'| <= 128), so the contracted
+          // x'^2 + y'^2 is still exactly symmetric; otherwise use IEEE scalar ops
+          if constexpr (sizeof(TIN) == 1) P[2] = fma2(X, X, mul2(Y, Y));
+          else P[2] = sumsq2(X, Y);
           P[3] = mul2(X, Y);
         } else {
           P[2] = mul2(X, X);
@@ -273,28 +279,39 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) {
         const u64 m1 = acc[0][jj], m2 = acc[1][jj];
-        u64 v1, v2, cv, den2;
+        // Everything below is symmetric in (ref, dist): Pm = m1 m2, Sm = m1 + m2 and
+        // Mm = m1^2 + m2^2 (IEEE scalar ops) are, and every further step uses only them.
+        const u64 Pm = mul2(m1, m2);
+        u64 v1, v2, cv, den2, Mm = 0ull;
         if constexpr (NM == 4) {
           // sigma1^2 + sigma2^2 = E[x^2 + y^2] - (m1^2 + m2^2), clamped as a sum
-          v1 = max0_2(sub2(acc[2][jj], sumsq2(m1, m2)));
+          Mm = sumsq2(m1, m2);
+          v1 = max0_2(sub2(acc[2][jj], Mm));
           v2 = 0ull;
-          cv = sub2(acc[3][jj], mul2(m1, m2));
+          cv = sub2(acc[3][jj], Pm);
           den2 = add2(v1, c2_2);
         } else {
           v1 = max0_2(sub2(acc[2][jj], mul2(m1, m1)));
           v2 = max0_2(sub2(acc[3][jj], mul2(m2, m2)));
-          cv = sub2(acc[NM - 1][jj], mul2(m1, m2));
+          cv = sub2(acc[NM - 1][jj], Pm);
           den2 = add2(add2(v1, v2), c2_2);
         }
         const u64 num2 = fma2(two2, cv, c2_2);
         const u64 cs = mul2(num2, rcp2(den2));
-        u64 l = 0ull, q = cs;
-        const u64 mu1 = add2(m1, shift2), mu2 = add2(m2, shift2);
+        u64 l = 0ull, q = cs, mu1 = 0ull, mu2 = 0ull;
         if (full_terms) {
-          const u64 num1 = fma2(add2(mu1, mu1), mu2, c1_2);
-          const u64 den1 = add2(sumsq2(mu1, mu2), c1_2);
+          // with mu = m + s (s = L/2): 2 mu1 mu2 + C1 = 2 Pm + T and mu1^2 + mu2^2 + C1 = Mm + T,
+          // T = 2 s Sm + 2 s^2 + C1 (no catastrophic cancellation: all terms share a sign)
+          if constexpr (NM != 4) Mm = sumsq2(m1, m2);
+          const u64 T = fma2(twoshift2, add2(m1, m2), c1b_2);
+          const u64 num1 = fma2(two2, Pm, T);
+          const u64 den1 = add2(Mm, T);
           l = mul2(num1, rcp2(den1));
           q = mul2(l, cs);
+        }
+        if (want_maps) {
+          mu1 = add2(m1, shift2);
+          mu2 = add2(m2, shift2);
         }
         const int col = ocol0 + jj;
         const bool valid = jj < ncol && (s == 1 || col % s == 0);
