@@ -21,6 +21,7 @@ inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a
 
 struct Plan {
   bool gauss = false;
+  bool box_block = false;
   bool box_int = false;
   bool wide = false;
   dim3 grid, block;
@@ -139,6 +140,22 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
   a.map_frame = a.map_plane * ((want & SSK_MAP_STATS) ? 5 : 3);
   a.wsums = nullptr;
   const bool integer = p->dtype == SSK_U8 || p->dtype == SSK_U16 || p->dtype == SSK_U32;
+  if (integer && box_block_supported(p->dtype, k, s, (double)k * k * stored_max * stored_max >= 4294967296.0,
+                                     stored_max)) {
+    // stride divides the window: block-sum kernel (warps of 248 new columns, ~16 anchor rows per
+    // segment: enough independent warps to keep HBM busy even for a handful of frames)
+    pl.box_block = true;
+    int seg_anchors = 16;
+    long long nseg = (pl.gh + seg_anchors - 1) / seg_anchors;
+    seg_anchors = (int)((pl.gh + nseg - 1) / nseg);
+    a.seg_anchors = seg_anchors;
+    nseg = (pl.gh + seg_anchors - 1) / seg_anchors;
+    const int nwarps = (p->w + 247) / 248;
+    pl.grid = dim3((nwarps + 3) / 4, (unsigned)nseg, p->n);
+    if (nseg > 65535) return SSK_E_ARG;
+    pl.nparts_per_frame = (size_t)pl.grid.x * pl.grid.y;
+    return SSK_OK;
+  }
   if (integer && k <= BX_THREADS) {
     pl.box_int = true;
     pl.wide = (double)k * k * stored_max * stored_max >= 4294967296.0;
@@ -184,6 +201,7 @@ int run_plan(Plan& pl, double* partials, void* maps, long long* wsums, cudaStrea
   pl.ba.partials = partials;
   pl.ba.maps = static_cast<double*>(maps);
   pl.ba.wsums = wsums;
+  if (pl.box_block) return launch_box_block(pl.ba, pl.grid, st);
   if (pl.box_int) return launch_box_int(pl.ba, pl.grid, pl.wide, st);
   return launch_box_float(pl.ba, pl.grid, pl.block, st);
 }

@@ -78,6 +78,8 @@ struct BoxArgs {
 size_t box_smem_bytes(const BoxArgs& a, bool wide);
 int launch_box_int(const BoxArgs& a, dim3 grid, bool wide, cudaStream_t st);
 int launch_box_float(const BoxArgs& a, dim3 grid, dim3 block, cudaStream_t st);
+bool box_block_supported(int dtype, int k, int s, bool wide, double stored_max);
+int launch_box_block(const BoxArgs& a, dim3 grid, cudaStream_t st);
 
 // ---------------- pyramid + MS-SSIM finalize ----------------
 struct PyramidArgs {

@@ -305,3 +305,22 @@ def test_downsample_shapes_and_dtypes(cuda, oracle, rng, h, w, kind):
     got2 = P.dyadic_downsample(got) if min(got.shape) >= 2 else None
     if got2 is not None:
         assert np.array_equal(got2, oracle.dyadic_downsample(want))
+
+
+@pytest.mark.parametrize("k,s,bd,h,w", [(8, 4, 10, 70, 300), (8, 4, 8, 64, 517), (4, 2, 8, 33, 65), (12, 4, 10, 50, 260),
+                                        (8, 8, 10, 40, 270), (16, 8, 8, 47, 300), (10, 2, 8, 31, 90), (4, 4, 12, 30, 80),
+                                        (16, 8, 12, 40, 100)])
+def test_block_box_path_bit_exact(cuda, oracle, rng, k, s, bd, h, w):
+    """Stride-divides-window rect path (block sums): int64 window sums and maps bit-exact."""
+    peak = (1 << bd) - 1
+    dt = np.uint8 if bd == 8 else np.uint16
+    a = rng.integers(0, peak + 1, (h, w)).astype(dt)
+    b = np.clip(a.astype(np.int64) + rng.integers(-40, 41, a.shape), 0, peak).astype(dt)
+    pair = engine.upload_pair(a, b, bd, gauss=False)
+    got = engine.window_sums(pair, k, s)[0].cpu().numpy()
+    assert np.array_equal(got, oracle.box_window_sums(a, b, k, s))
+    cfg = P.SsimConfig(bit_depth=bd, window=P.WindowSpec.rectangular(k, stride=s))
+    maps = P.ssim_map(P.LumaPlane(a, bd), P.LumaPlane(b, bd), cfg)
+    want = oracle.ssim_maps(a, b, shape="rect", k=k, stride=s, bit_depth=bd)
+    assert np.array_equal(maps.q_map.values, want[2]) and np.array_equal(maps.l_map.values, want[0])
+    assert abs(P.ssim_score(P.LumaPlane(a, bd), P.LumaPlane(b, bd), cfg) - float(want[2].mean())) < 1e-12

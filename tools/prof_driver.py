@@ -2,7 +2,7 @@
 
   --mode step : 3 full bench steps (64x 1080p SSIM + 5-scale MS-SSIM) -> launch list / shares
   --mode l0   : the level-0 fused Gaussian SSIM kernel over the 64-frame batch, 3 launches
-  --mode box  : config-4 shape: rect 8 stride 4 on 10-bit 4K u16, 8 frames, 3 launches
+  --mode box  : config-4 shape: rect 8 stride 4 on 10-bit 4K u16, 32 frames, 3 launches
 """
 
 from __future__ import annotations
@@ -29,8 +29,8 @@ def main() -> None:
     dev = torch.device("cuda", 0)
     if args.mode == "box":
         pairs = [synth.config4_pair(i, 2160, 3840) for i in range(2)]
-        ref = np.stack([pairs[i % 2][0] for i in range(8)])
-        dist = np.stack([pairs[i % 2][1] for i in range(8)])
+        ref = np.stack([pairs[i % 2][0] for i in range(32)])
+        dist = np.stack([pairs[i % 2][1] for i in range(32)])
         cfg = P.SsimConfig(bit_depth=10, window=P.WindowSpec.rectangular(8, stride=4), engine="integral")
         r, d = torch.from_numpy(ref).to(dev), torch.from_numpy(dist).to(dev)
         for _ in range(args.reps):
