@@ -88,6 +88,9 @@ __device__ __forceinline__ u64 max0_2(u64 v) {
 }
 
 constexpr int G = GS_G;                       // output rows per chunk
+#ifndef GS_MINB
+#define GS_MINB (NM == 4 ? 4 : 3)  // 4 CTAs/SM measured faster than 3 with more registers
+#endif
 constexpr int VP = GS_VCOLS * 8 + 8;          // V-row pitch (bytes): a half warp's 8 rows x 2 column groups hit distinct banks
 
 __host__ __device__ constexpr int tw_of(int k) { return ((GS_VCOLS - (k - 1)) / 16) * 16; }
@@ -372,7 +375,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
 }
 
 template <int K, typename TIN, int NM>
-__global__ void __launch_bounds__(GS_THREADS, NM == 4 ? 4 : 3) gauss_pair_kernel(const __grid_constant__ GaussArgs a) {
+__global__ void __launch_bounds__(GS_THREADS, GS_MINB) gauss_pair_kernel(const __grid_constant__ GaussArgs a) {
   gauss_body<K, TIN, NM>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.x, gridDim.y);
 }
 

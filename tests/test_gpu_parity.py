@@ -324,3 +324,86 @@ def test_block_box_path_bit_exact(cuda, oracle, rng, k, s, bd, h, w):
     want = oracle.ssim_maps(a, b, shape="rect", k=k, stride=s, bit_depth=bd)
     assert np.array_equal(maps.q_map.values, want[2]) and np.array_equal(maps.l_map.values, want[0])
     assert abs(P.ssim_score(P.LumaPlane(a, bd), P.LumaPlane(b, bd), cfg) - float(want[2].mean())) < 1e-12
+
+
+# --- deeper pyramid / dtype coverage -----------------------------------------
+
+@pytest.mark.parametrize("bd,levels,window", [
+    (10, 5, P.WindowSpec.gaussian(1.5)),   # u16 input, u32 pyramid levels
+    (12, 4, P.WindowSpec.rectangular(7)),  # u16 input, exact integer pyramid, fp64 epilogue
+    (16, 3, P.WindowSpec.gaussian(1.0)),   # full 16-bit range
+    (8, 5, P.WindowSpec.gaussian(1.5, stride=2)),
+])
+def test_msssim_deep_inputs_vs_oracle(cuda, oracle, rng, bd, levels, window):
+    from paper_2101_06354_b200 import synth
+
+    h, w = 11 * 16 + 9, 11 * 16 + 37
+    peak = (1 << bd) - 1
+    base = synth.inv_f_noise(rng, h, w, float(peak))
+    a = base.astype(np.uint16 if bd > 8 else np.uint8)
+    b = np.clip(base + rng.normal(0, peak / 40, base.shape), 0, peak).round().astype(a.dtype)
+    cfg = P.SsimConfig(bit_depth=bd, window=window)
+    win = dict(shape=window.shape, k=window.k, stride=window.stride, sigma=window.sigma, bit_depth=bd)
+    got = P.scale_scores(P.LumaPlane(a, bd), P.LumaPlane(b, bd), cfg, levels)
+    want = oracle.scale_scores(a, b, levels, **win)
+    tol = 1e-12 if window.shape == "rect" else 1e-5
+    assert np.max(np.abs(np.array(got) - np.array(want))) < tol
+
+
+def test_msssim_float_input_vs_oracle(cuda, oracle, rng):
+    a = rng.uniform(0, 255, (100, 120))
+    b = np.clip(a + rng.normal(0, 8, a.shape), 0, 255)
+    for window, tol in ((P.WindowSpec.rectangular(5), 1e-9), (P.WindowSpec.gaussian(1.5), 1e-5)):
+        cfg = P.SsimConfig(window=window)
+        win = dict(shape=window.shape, k=window.k, sigma=window.sigma)
+        got = P.msssim(P.LumaPlane(a), P.LumaPlane(b), cfg, P.MultiscaleSpec.product(3))
+        assert abs(got - oracle.msssim(a, b, 3, **win)) < tol
+
+
+def test_batch_api_odd_counts_misaligned_widths_and_color(cuda, oracle, rng):
+    import torch
+
+    n, h, w = 5, 41, 77  # odd n (last frame pair half empty), width not a multiple of 16
+    a = rng.integers(0, 256, (n, h, w)).astype(np.uint8)
+    b = np.clip(a.astype(int) + rng.integers(-30, 31, a.shape), 0, 255).astype(np.uint8)
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    got = P.ssim_batch(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), cfg).cpu().numpy()
+    want = np.array([oracle.ssim_score(a[i], b[i], shape="gauss", k=11, sigma=1.5) for i in range(n)])
+    assert np.max(np.abs(got - want)) < 1e-5
+    # channel-wise color on device batches (4:2:0 planes at their own resolution)
+    ys = [torch.from_numpy(a).cuda(), torch.from_numpy(a[:, ::2, ::2].copy()).cuda(), torch.from_numpy(a[:, 1::2, ::2].copy()).cuda()]
+    ds = [torch.from_numpy(b).cuda(), torch.from_numpy(b[:, ::2, ::2].copy()).cuda(), torch.from_numpy(b[:, 1::2, ::2].copy()).cuda()]
+    rc = P.SsimConfig(window=P.WindowSpec.rectangular(5))
+    cw = P.color_batch(ys, ds, rc, alpha=-0.3, beta=-0.3).cpu().numpy()
+    fx = P.color_batch(ys, ds, rc, weights=(0.8, 0.1, 0.1)).cpu().numpy()
+    for i in range(n):
+        sc = oracle.channel_scores([t[i].cpu().numpy() for t in ys], [t[i].cpu().numpy() for t in ds], shape="rect", k=5)
+        assert abs(cw[i] - oracle.channelwise(sc, -0.3, -0.3)) < 1e-12
+        assert abs(fx[i] - oracle.fixed_weight(sc, (0.8, 0.1, 0.1))) < 1e-12
+
+
+def test_host_batch_scorer_matches_device_batch(cuda, rng):
+    import torch
+
+    n = 11
+    a = rng.integers(0, 256, (n, 96, 130)).astype(np.uint8)
+    b = np.clip(a.astype(int) + rng.integers(-20, 21, a.shape), 0, 255).astype(np.uint8)
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    spec = P.MultiscaleSpec.product(3)
+    scorer = P.HostBatchScorer(cfg, spec, mode="both", chunk=4)
+    ms, ss = scorer(torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory())
+    ms_dev, terms = P.msssim_batch(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), cfg, spec, with_ssim=True)
+    assert np.array_equal(ms, ms_dev.cpu().numpy())
+    assert np.array_equal(ss[:, 0], terms.score.cpu().numpy())
+    assert scorer.h2d_bytes == 2 * a.nbytes
+
+
+def test_sequence_scorer_multiscale_and_temporal_pooler(cuda, oracle, rng):
+    frames = [(rng.integers(0, 256, (64, 80)).astype(np.uint8), rng.integers(0, 256, (64, 80)).astype(np.uint8))
+              for _ in range(7)]
+    cfg = P.SsimConfig(window=P.WindowSpec.rectangular(5), multiscale=P.MultiscaleSpec.product(3), temporal_pool="hm")
+    res = P.score_sequence([f[0] for f in frames], [f[1] for f in frames], cfg, batch_frames=3)
+    want = np.array([oracle.msssim(a, b, 3, shape="rect", k=5) for a, b in frames])
+    assert np.max(np.abs(res.scores - want)) < 1e-12
+    assert abs(res.pooled - P.pool_temporal(want, "hm")) < 1e-12
+    assert all(r.am is None for r in res.records)
