@@ -3,12 +3,22 @@
 // inside the calls (all scratch comes from the caller's workspace).
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
 #include "kernels.h"
 
 namespace ssk {
+namespace gk {
+int gauss_ws_level() {
+  static const int v = [] {
+    const char* e = std::getenv("SSK_GAUSS_WS");  // warp-specialised K1 (default on; 0 = classic)
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+}  // namespace gk
 
 static std::atomic<unsigned long long> g_launches{0};
 void note_launch(int count) { g_launches.fetch_add((unsigned long long)count); }

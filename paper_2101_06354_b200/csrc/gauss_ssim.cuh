@@ -81,6 +81,12 @@ __device__ __forceinline__ u64 rcp2(u64 v) {
   upk(v, a, b);
   return pk(rcp_approx(a), rcp_approx(b));
 }
+__device__ __forceinline__ u64 add_rn2(u64 a, u64 b) {  // two IEEE scalar adds, never contracted
+  float a0, a1, b0, b1;
+  upk(a, a0, a1);
+  upk(b, b0, b1);
+  return pk(__fadd_rn(a0, b0), __fadd_rn(a1, b1));
+}
 __device__ __forceinline__ u64 max0_2(u64 v) {
   float a, b;
   upk(v, a, b);
@@ -88,6 +94,8 @@ __device__ __forceinline__ u64 max0_2(u64 v) {
 }
 
 constexpr int G = GS_G;                       // output rows per chunk
+int gauss_ws_level();                         // capi.cu: SSK_GAUSS_WS environment switch (default 1)
+inline bool gauss_ws_enabled() { return gauss_ws_level() >= 1; }
 #ifndef GS_MINB
 #define GS_MINB (NM == 4 ? 4 : 3)  // 4 CTAs/SM measured faster than 3 with more registers
 #endif
@@ -123,7 +131,18 @@ __device__ __forceinline__ u64 sumsq2(u64 x, u64 y) {
 // applied to the sum (differs from per-variance clamping only by fp32 rounding
 // residue of flat windows).  NM = 5 (x, y, x^2, y^2, xy) serves the statistics
 // maps of local_statistics.
-template <int K, typename TIN, int NM>
+// WS = warp-specialised variant: 8 warps per CTA, warps 0-3 run the V pass
+// (producers) and warps 4-7 the H pass + epilogue (consumers) over a double-
+// buffered V tile, synchronised by named barriers, so the two phases overlap
+// instead of alternating behind CTA-wide barriers.
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+template <int K, typename TIN, int NM, bool WS>
 __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, const int seg, const int pair,
                                            const int nstrips, const int nseg) {
   constexpr int TW = tw_of(K);
@@ -136,11 +155,12 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
   constexpr int NP = 8 + K - 1;                     // V values read per H item
   static_assert(TWI <= GS_THREADS, "strip wider than the CTA");
 
+  constexpr int NT = WS ? 2 * GS_THREADS : GS_THREADS;  // threads per CTA
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* raw = smem;                        // [RR][4][RB]
-  unsigned char* vbuf = smem + RR * 4 * RB;         // [NM][G][VP]
+  unsigned char* vbuf0 = smem + RR * 4 * RB;        // [WS ? 2 : 1][NM][G][VP]
   __shared__ float s_taps[32];
-  __shared__ double s_red[(GS_THREADS / 32) * 6];
+  __shared__ double s_red[(2 * GS_THREADS / 32) * 6];
 
   const int tid = threadIdx.x;
   const int f0 = 2 * pair;
@@ -156,7 +176,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
   const long long fo0 = (long long)f0 * a.frame_pitch_b, fo1 = (long long)f1 * a.frame_pitch_b;
   const int row_bytes_left = (a.w - c0) * ES;
 
-  auto stage_rows = [&](int r_lo, int r_hi) {
+  auto stage_rows = [&](int r_lo, int r_hi) {  // issued by the GS_THREADS V-pass threads
     r_hi = min(r_hi, in_end);
     const int total = (r_hi - r_lo) * 4 * NCH;
     for (int i = tid; i < total; i += GS_THREADS) {
@@ -177,7 +197,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
     cp_async_commit();
   };
 
-  stage_rows(y0, y0 + G + K - 1);
+  if (tid < GS_THREADS) stage_rows(y0, y0 + G + K - 1);
   if (tid < 32) s_taps[tid] = a.taps[tid];
   __syncthreads();
   u64 w2[NH];
@@ -188,7 +208,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
   const u64 bias2 = pk(a.conv_bias, a.conv_bias);
   const u64 shift2 = pk(a.shift, a.shift);
   const u64 c1_2 = pk(a.c1, a.c1), c2_2 = pk(a.c2, a.c2);
-  const u64 two2 = pk(2.f, 2.f);
+  const u64 two2 = pk(2.f, 2.f), one2 = pk(1.f, 1.f);
   const u64 twoshift2 = pk(2.f * a.shift, 2.f * a.shift);
   const float c1b = 2.f * a.shift * a.shift + a.c1;  // 2 s^2 + C1 (exact for s = 2^(bd-1))
   const u64 c1b_2 = pk(c1b, c1b);
@@ -198,18 +218,11 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
   const int wo = a.wo;
 
   double tq0 = 0.0, tl0 = 0.0, tc0 = 0.0, tq1 = 0.0, tl1 = 0.0, tc1 = 0.0;
-  const int hg = tid % G, hj = tid / G;  // H item: output row hg of the chunk, columns 8*hj..8*hj+7
+  const int htid = WS ? tid - GS_THREADS : tid;
+  const int hg = htid % G, hj = htid / G;  // H item: output row hg of the chunk, columns 8*hj..8*hj+7
 
-  for (int c = 0; c < nchunks; ++c) {
-    if (c + 1 < nchunks) {
-      stage_rows(y0 + (c + 1) * G + K - 1, y0 + (c + 2) * G + K - 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-
-    // ---------------- V pass: thread = input column ----------------
+  // ---------------- V pass: thread = input column ----------------
+  auto vpass = [&](const int c, unsigned char* vbuf) {
     if (tid < TWI && c0 + tid < a.w) {
       u64 acc[NM][G];
 #pragma unroll
@@ -254,9 +267,10 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
         for (int r = 0; r < G; ++r)
           *reinterpret_cast<u64*>(vbuf + (m * G + r) * VP + tid * 8) = acc[m][r];
     }
-    __syncthreads();
+  };
 
-    // ---------------- H pass + epilogue: thread = (row, 8 columns) ----------------
+  // ---------------- H pass + epilogue: thread = (row, 8 columns) ----------------
+  auto hpass = [&](const int c, const unsigned char* vbuf) {
     const int orow = y0 + c * G + hg;
     const int ocol0 = c0 + 8 * hj;
     if (8 * hj < TW && ocol0 < wo && orow < y1 && (s == 1 || orow % s == 0)) {
@@ -285,18 +299,19 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
         // Everything below is symmetric in (ref, dist): Pm = m1 m2, Sm = m1 + m2 and
         // Mm = m1^2 + m2^2 (IEEE scalar ops) are, and every further step uses only them.
         const u64 Pm = mul2(m1, m2);
+        const u64 nm2 = sub2(0ull, m2);  // exact negation; cov = fma(m1, -m2, E[xy]) stays one rounding
         u64 v1, v2, cv, den2, Mm = 0ull;
         if constexpr (NM == 4) {
           // sigma1^2 + sigma2^2 = E[x^2 + y^2] - (m1^2 + m2^2), clamped as a sum
           Mm = sumsq2(m1, m2);
           v1 = max0_2(sub2(acc[2][jj], Mm));
           v2 = 0ull;
-          cv = sub2(acc[3][jj], Pm);
+          cv = fma2(m1, nm2, acc[3][jj]);
           den2 = add2(v1, c2_2);
         } else {
           v1 = max0_2(sub2(acc[2][jj], mul2(m1, m1)));
           v2 = max0_2(sub2(acc[3][jj], mul2(m2, m2)));
-          cv = sub2(acc[NM - 1][jj], Pm);
+          cv = fma2(m1, nm2, acc[NM - 1][jj]);
           den2 = add2(add2(v1, v2), c2_2);
         }
         const u64 num2 = fma2(two2, cv, c2_2);
@@ -319,11 +334,14 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
         const int col = ocol0 + jj;
         const bool valid = jj < ncol && (s == 1 || col % s == 0);
         if (valid) {
+          // sums as explicit FFMA2 x*1 + acc: ptxas contracts a mul.f32x2 feeding an
+          // add.f32x2 even with .rn, which would make a term's rounding depend on
+          // whether it is also used elsewhere (i.e. on the requested outputs)
           if (full_terms) {
-            sq = add2(sq, q);
-            sl = add2(sl, l);
+            sq = fma2(q, one2, sq);
+            sl = fma2(l, one2, sl);
           }
-          scs = add2(scs, cs);
+          scs = fma2(cs, one2, scs);
           if (want_maps) {
             const long long idx = (long long)(orow / s) * a.gw + (col / s);
             float lo, hi;
@@ -354,6 +372,44 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
       tc0 += lo;
       tc1 += hi;
     }
+  };
+
+  if constexpr (!WS) {
+    for (int c = 0; c < nchunks; ++c) {
+      if (c + 1 < nchunks) {
+        stage_rows(y0 + (c + 1) * G + K - 1, y0 + (c + 2) * G + K - 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      vpass(c, vbuf0);
+      __syncthreads();
+      hpass(c, vbuf0);
+    }
+  } else {
+    constexpr int VBYTES = NM * G * VP;
+    if (tid < GS_THREADS) {  // producers
+      for (int c = 0; c < nchunks; ++c) {
+        if (c + 1 < nchunks) {
+          stage_rows(y0 + (c + 1) * G + K - 1, y0 + (c + 2) * G + K - 1);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        named_sync(1, GS_THREADS);                             // chunk c's raw rows visible
+        if (c >= 2) named_sync(4 + (c & 1), 2 * GS_THREADS);   // consumers released this buffer
+        vpass(c, vbuf0 + (c & 1) * VBYTES);
+        named_arrive(2 + (c & 1), 2 * GS_THREADS);             // buffer full
+        named_sync(1, GS_THREADS);                             // raw rows of chunk c no longer read
+      }
+    } else {  // consumers
+      for (int c = 0; c < nchunks; ++c) {
+        named_sync(2 + (c & 1), 2 * GS_THREADS);
+        hpass(c, vbuf0 + (c & 1) * VBYTES);
+        if (c + 2 < nchunks) named_arrive(4 + (c & 1), 2 * GS_THREADS);
+      }
+    }
   }
 
   double v[6] = {tq0, tl0, tc0, tq1, tl1, tc1};
@@ -367,7 +423,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
   if (tid < 6 && (tid < 3 || has1)) {
     double t = 0.0;
 #pragma unroll
-    for (int wi = 0; wi < GS_THREADS / 32; ++wi) t += s_red[wi * 6 + tid];
+    for (int wi = 0; wi < NT / 32; ++wi) t += s_red[wi * 6 + tid];
     const int fr = tid < 3 ? f0 : f1;
     const long long part = ((long long)fr * nseg + seg) * nstrips + strip;
     a.partials[part * 3 + (tid % 3)] = t;
@@ -376,21 +432,27 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
 
 template <int K, typename TIN, int NM>
 __global__ void __launch_bounds__(GS_THREADS, GS_MINB) gauss_pair_kernel(const __grid_constant__ GaussArgs a) {
-  gauss_body<K, TIN, NM>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.x, gridDim.y);
+  gauss_body<K, TIN, NM, false>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.x, gridDim.y);
+}
+
+template <int K, typename TIN, int NM>
+__global__ void __launch_bounds__(2 * GS_THREADS, 2) gauss_ws_kernel(const __grid_constant__ GaussArgs a) {
+  gauss_body<K, TIN, NM, true>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.x, gridDim.y);
 }
 
 // All pyramid levels of one sample type in one launch: blockIdx.x enumerates the
 // (level, segment, strip) tiles, so the small coarse levels share the GPU with
 // each other instead of each launching a few dozen CTAs.
-template <int K, typename TIN, int NM>
-__global__ void __launch_bounds__(GS_THREADS, NM == 4 ? 4 : 3) gauss_levels_kernel(const __grid_constant__ GaussLevels p) {
+template <int K, typename TIN, int NM, bool WS>
+__global__ void __launch_bounds__(WS ? 2 * GS_THREADS : GS_THREADS, WS ? 2 : 4)
+    gauss_levels_kernel(const __grid_constant__ GaussLevels p) {
   int lv = 0;
 #pragma unroll
   for (int i = 1; i < GS_MAX_LEVELS; ++i)
     if (i < p.nlev && (int)blockIdx.x >= p.cta_off[i]) lv = i;
   const int local = blockIdx.x - p.cta_off[lv];
   const int ns = p.nstrips[lv];
-  gauss_body<K, TIN, NM>(p.lv[lv], local % ns, local / ns, blockIdx.z, ns, p.nseg[lv]);
+  gauss_body<K, TIN, NM, WS>(p.lv[lv], local % ns, local / ns, blockIdx.z, ns, p.nseg[lv]);
 }
 
 template <int K, typename TIN, int NM>
@@ -401,7 +463,19 @@ inline size_t smem_bytes() {
 }
 
 template <int K, typename TIN, int NM>
+int launch_ws(const GaussArgs& a, dim3 grid, cudaStream_t st) {
+  auto fn = gauss_ws_kernel<K, TIN, NM>;
+  const size_t smem = smem_bytes<K, TIN, NM>() + (size_t)NM * G * VP;  // second V buffer
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SSK_E_CUDA;
+  fn<<<grid, 2 * GS_THREADS, smem, st>>>(a);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+}
+
+template <int K, typename TIN, int NM>
 int launch_nm(const GaussArgs& a, dim3 grid, cudaStream_t st) {
+  if (NM == 4 && gauss_ws_enabled()) return launch_ws<K, TIN, NM>(a, grid, st);
   auto fn = gauss_pair_kernel<K, TIN, NM>;
   const size_t smem = smem_bytes<K, TIN, NM>();
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -419,11 +493,14 @@ int launch_one(const GaussArgs& a, dim3 grid, cudaStream_t st) {
 
 template <int K, typename TIN>
 int launch_levels_one(const GaussLevels& p, dim3 grid, cudaStream_t st) {
-  auto fn = gauss_levels_kernel<K, TIN, 4>;
-  const size_t smem = smem_bytes<K, TIN, 4>();
+  // the coarse levels stay on the classic (non-specialised) kernel: measured faster there
+  // (small tiles, 3-4 CTAs/SM); SSK_GAUSS_WS=2 forces the warp-specialised variant
+  const bool ws = gauss_ws_level() >= 2;
+  auto fn = ws ? gauss_levels_kernel<K, TIN, 4, true> : gauss_levels_kernel<K, TIN, 4, false>;
+  const size_t smem = smem_bytes<K, TIN, 4>() + (ws ? (size_t)4 * G * VP : 0);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SSK_E_CUDA;
-  fn<<<grid, GS_THREADS, smem, st>>>(p);
+  fn<<<grid, ws ? 2 * GS_THREADS : GS_THREADS, smem, st>>>(p);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
 }
