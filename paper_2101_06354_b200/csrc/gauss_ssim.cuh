@@ -94,6 +94,9 @@ __device__ __forceinline__ u64 max0_2(u64 v) {
 }
 
 constexpr int G = GS_G;                       // output rows per chunk
+#ifndef GS_NBUF
+#define GS_NBUF 3                             // V tiles in flight in the warp-specialised kernel
+#endif
 int gauss_ws_level();                         // capi.cu: SSK_GAUSS_WS environment switch (default 1)
 inline bool gauss_ws_enabled() { return gauss_ws_level() >= 1; }
 #ifndef GS_MINB
@@ -389,7 +392,10 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
     }
   } else {
     constexpr int VBYTES = NM * G * VP;
+    // GS_NBUF V tiles in flight; named barriers 2..2+NBUF-1 = "tile b full",
+    // 2+NBUF.. = "tile b free"; barrier 1 = producer-internal
     if (tid < GS_THREADS) {  // producers
+      int b = 0;
       for (int c = 0; c < nchunks; ++c) {
         if (c + 1 < nchunks) {
           stage_rows(y0 + (c + 1) * G + K - 1, y0 + (c + 2) * G + K - 1);
@@ -397,17 +403,20 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
         } else {
           cp_async_wait<0>();
         }
-        named_sync(1, GS_THREADS);                             // chunk c's raw rows visible
-        if (c >= 2) named_sync(4 + (c & 1), 2 * GS_THREADS);   // consumers released this buffer
-        vpass(c, vbuf0 + (c & 1) * VBYTES);
-        named_arrive(2 + (c & 1), 2 * GS_THREADS);             // buffer full
-        named_sync(1, GS_THREADS);                             // raw rows of chunk c no longer read
+        named_sync(1, GS_THREADS);                                   // chunk c's raw rows visible
+        if (c >= GS_NBUF) named_sync(2 + GS_NBUF + b, 2 * GS_THREADS);  // consumers released tile b
+        vpass(c, vbuf0 + b * VBYTES);
+        named_arrive(2 + b, 2 * GS_THREADS);                         // tile b full
+        named_sync(1, GS_THREADS);                                   // raw rows of chunk c no longer read
+        b = b + 1 == GS_NBUF ? 0 : b + 1;
       }
     } else {  // consumers
+      int b = 0;
       for (int c = 0; c < nchunks; ++c) {
-        named_sync(2 + (c & 1), 2 * GS_THREADS);
-        hpass(c, vbuf0 + (c & 1) * VBYTES);
-        if (c + 2 < nchunks) named_arrive(4 + (c & 1), 2 * GS_THREADS);
+        named_sync(2 + b, 2 * GS_THREADS);
+        hpass(c, vbuf0 + b * VBYTES);
+        if (c + GS_NBUF < nchunks) named_arrive(2 + GS_NBUF + b, 2 * GS_THREADS);
+        b = b + 1 == GS_NBUF ? 0 : b + 1;
       }
     }
   }
@@ -465,7 +474,7 @@ inline size_t smem_bytes() {
 template <int K, typename TIN, int NM>
 int launch_ws(const GaussArgs& a, dim3 grid, cudaStream_t st) {
   auto fn = gauss_ws_kernel<K, TIN, NM>;
-  const size_t smem = smem_bytes<K, TIN, NM>() + (size_t)NM * G * VP;  // second V buffer
+  const size_t smem = smem_bytes<K, TIN, NM>() + (size_t)(GS_NBUF - 1) * NM * G * VP;  // extra V tiles
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SSK_E_CUDA;
   fn<<<grid, 2 * GS_THREADS, smem, st>>>(a);
@@ -497,7 +506,7 @@ int launch_levels_one(const GaussLevels& p, dim3 grid, cudaStream_t st) {
   // (small tiles, 3-4 CTAs/SM); SSK_GAUSS_WS=2 forces the warp-specialised variant
   const bool ws = gauss_ws_level() >= 2;
   auto fn = ws ? gauss_levels_kernel<K, TIN, 4, true> : gauss_levels_kernel<K, TIN, 4, false>;
-  const size_t smem = smem_bytes<K, TIN, 4>() + (ws ? (size_t)4 * G * VP : 0);
+  const size_t smem = smem_bytes<K, TIN, 4>() + (ws ? (size_t)(GS_NBUF - 1) * 4 * G * VP : 0);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SSK_E_CUDA;
   fn<<<grid, ws ? 2 * GS_THREADS : GS_THREADS, smem, st>>>(p);
