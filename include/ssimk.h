@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SSK_ABI_VERSION 2
+#define SSK_ABI_VERSION 3
 
 /* sample storage types */
 enum {
@@ -172,6 +172,38 @@ int ssk_downsample(const ssk_planes* src, void* d_dst_ref, void* d_dst_dist, int
 int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, const double* exponents,
                int aggregation, double* d_level_means, double* d_scores, double* d_ssim_sums,
                void* d_workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * SSIM-3D rolling volumes (src/spatiotemporal.py:28-207).  The caller owns the
+ * five temporal-sum planes [5][h][pitch] (x, y, x^2, y^2, xy summed over the
+ * last `depth` frame pairs): int64 for integer samples (exact, no drift, so the
+ * reference's periodic refresh is a no-op) or float64 for float samples.
+ */
+typedef struct ssk_volume {
+  void* planes;
+  int32_t is_float;     /* 0: int64 planes (u8/u16 frames), 1: float64 planes (f64 frames) */
+  int32_t h, w;
+  int32_t depth;        /* frames currently summed (1..Kt)                  */
+  int64_t pitch;        /* elements between rows of one plane               */
+} ssk_volume;
+
+/* mode 0: planes = terms(new); 1: planes += terms(new);
+ * 2: planes = planes - terms(old) + terms(new)  (RollingVolume.push, :60-97).
+ * Frames: device [h][src_row_pitch] of `dtype` (SSK_U8/SSK_U16 for int64 planes,
+ * SSK_F64 for float64 planes). */
+int ssk_volume_update(const ssk_volume* v, const void* new_ref, const void* new_dist, const void* old_ref,
+                      const void* old_dist, int dtype, int64_t src_row_pitch, int mode, void* stream);
+/* float64 planes only: recompute from `count` buffered frame pairs, oldest first
+ * (RollingVolume._refresh / direct_sums, :99-115); refs/dists: HOST arrays of
+ * device pointers, count <= 64. */
+int ssk_volume_refresh(const ssk_volume* v, const void* const* refs, const void* const* dists, int count,
+                       int dtype, int64_t src_row_pitch, void* stream);
+size_t ssk_volume_workspace_bytes(const ssk_volume* v, const ssk_window* win);
+/* k x k x depth window SSIM over the volume (RollingVolume.local_statistics +
+ * ssim3d_map, :116-149): rect windows only; area = k*k*depth.  d_sums [1][3]
+ * as in ssk_ssim; optional float64 maps (SSK_MAP_TERMS / SSK_MAP_STATS). */
+int ssk_volume_ssim(const ssk_volume* v, const ssk_window* win, int want, double* d_sums, void* d_maps,
+                    void* d_workspace, size_t workspace_bytes, void* stream);
 
 /* Number of kernels this library has launched since load (for bench.py). */
 uint64_t ssk_launch_count(void);

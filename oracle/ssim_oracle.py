@@ -229,3 +229,81 @@ def channelwise(scores, alpha: float, beta: float) -> float:
 
 def pool_temporal_am(scores) -> float:
     return float(np.asarray(scores, dtype=np.float64).reshape(-1).mean())
+
+
+# ---------------------------------------------------------------------------
+# SSIM-3D rolling volumes (src/spatiotemporal.py:28-207)
+# ---------------------------------------------------------------------------
+
+class RollingSums:
+    """Float64 rolling temporal sums exactly as the reference keeps them."""
+
+    def __init__(self, kt: int, refresh_interval: int = 300):
+        self.kt, self.refresh_interval = kt, refresh_interval
+        self.buffer: list = []
+        self.sums = None
+        self.pushes = 0
+
+    @staticmethod
+    def _terms(a, b):
+        return [a, b, a * a, b * b, a * b]
+
+    def push(self, ref, dist):
+        a = np.asarray(ref, dtype=np.float64)
+        b = np.asarray(dist, dtype=np.float64)
+        new = self._terms(a, b)
+        if self.sums is None or self.kt == 1:
+            self.sums = [t.copy() for t in new]
+        elif len(self.buffer) == self.kt:
+            old = self._terms(*self.buffer[0])
+            for s, n_, o in zip(self.sums, new, old):
+                s -= o
+                s += n_
+        else:
+            for s, n_ in zip(self.sums, new):
+                s += n_
+        if len(self.buffer) == self.kt:
+            self.buffer.pop(0)
+        self.buffer.append((a, b))
+        self.pushes += 1
+        if self.refresh_interval and self.pushes % self.refresh_interval == 0:
+            fresh = [np.zeros(a.shape) for _ in range(5)]
+            for x, y in self.buffer:
+                for s, t in zip(fresh, self._terms(x, y)):
+                    s += t
+            self.sums = fresh
+
+    def stats(self, k: int, stride: int = 1):
+        grids = [grid_window_sums(sat(s), k, stride) for s in self.sums]
+        return moments_from_sums(*grids, area=float(k * k * len(self.buffer)))
+
+
+def ssim3d_series(ref_frames, dist_frames, kt: int, k: int = 11, stride: int = 1, bit_depth: int = 8,
+                  refresh_interval: int = 300) -> list:
+    c1, c2 = constants(bit_depth)
+    vol = RollingSums(kt, refresh_interval)
+    out = []
+    for a, b in zip(ref_frames, dist_frames):
+        vol.push(a, b)
+        out.append(float(term_maps(*vol.stats(k, stride), c1, c2)[2].mean()))
+    return out
+
+
+def msssim3d(ref_frames, dist_frames, kt: int, levels: int = 5, aggregation: str = "product", exponents=None,
+             k: int = 11, stride: int = 1, bit_depth: int = 8) -> list:
+    if exponents is None:
+        exponents = STANDARD_EXPONENTS[:levels]
+    c1, c2 = constants(bit_depth)
+    vols = [RollingSums(kt) for _ in range(levels)]
+    out = []
+    for a, b in zip(ref_frames, dist_frames):
+        cur_a, cur_b = a, b
+        per = []
+        for lv in range(levels):
+            if lv:
+                cur_a, cur_b = dyadic_downsample(cur_a), dyadic_downsample(cur_b)
+            vols[lv].push(cur_a, cur_b)
+            _, cs_map, q = term_maps(*vols[lv].stats(k, stride), c1, c2)
+            per.append(float((q if lv == levels - 1 else cs_map).mean()))
+        out.append(combine_scale_scores(per, aggregation, exponents))
+    return out

@@ -60,6 +60,7 @@ from .scoring import (
     weber_luminance_term,
 )
 from .video import SequenceScorer, gather_frame_scores, score_sequence, shard_bounds
+from .volume import REFRESH_INTERVAL, RollingVolume, msssim3d, push_frame, ssim3d_map, ssim3d_series
 
 __version__ = "0.1.0"
 
@@ -85,4 +86,6 @@ __all__ = [
     # batched device API / sequences / multi-GPU
     "FrameTerms", "HostBatchScorer", "color_batch", "msssim_batch", "ssim_batch", "ssim_terms_batch",
     "SequenceScorer", "gather_frame_scores", "score_sequence", "shard_bounds",
+    # spatio-temporal (SSIM-3D)
+    "REFRESH_INTERVAL", "RollingVolume", "msssim3d", "push_frame", "ssim3d_map", "ssim3d_series",
 ]

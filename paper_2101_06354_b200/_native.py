@@ -32,7 +32,7 @@ RECT, GAUSS = 1, 2
 WANT_Q, WANT_L, WANT_CS, MAP_TERMS, MAP_STATS = 1, 2, 4, 8, 16
 E_ARG, E_WINDOW, E_SHAPE, E_WORKSPACE, E_ALIGN, E_CUDA, E_LEVELS, E_TOO_SMALL = range(-1, -9, -1)
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 EXPORTED_SYMBOLS = (
     "ssk_abi_version",
@@ -44,6 +44,10 @@ EXPORTED_SYMBOLS = (
     "ssk_integral_tables",
     "ssk_downsample",
     "ssk_msssim",
+    "ssk_volume_update",
+    "ssk_volume_refresh",
+    "ssk_volume_workspace_bytes",
+    "ssk_volume_ssim",
     "ssk_launch_count",
     "ssk_probe_fp32_tflops",
 )
@@ -61,6 +65,17 @@ class Planes(ctypes.Structure):
         ("bit_depth", ctypes.c_int32),
         ("row_pitch", ctypes.c_int64),
         ("frame_pitch", ctypes.c_int64),
+    ]
+
+
+class Volume(ctypes.Structure):
+    _fields_ = [
+        ("planes", ctypes.c_void_p),
+        ("is_float", ctypes.c_int32),
+        ("h", ctypes.c_int32),
+        ("w", ctypes.c_int32),
+        ("depth", ctypes.c_int32),
+        ("pitch", ctypes.c_int64),
     ]
 
 
@@ -110,6 +125,15 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         lib.ssk_downsample.argtypes = [pP, vp, vp, i32, i64, i64, vp]
         lib.ssk_msssim.restype = i32
         lib.ssk_msssim.argtypes = [pP, pW, i32, ctypes.POINTER(ctypes.c_double), i32, vp, vp, vp, vp, sz, vp]
+        pV = ctypes.POINTER(Volume)
+        lib.ssk_volume_update.restype = i32
+        lib.ssk_volume_update.argtypes = [pV, vp, vp, vp, vp, i32, i64, i32, vp]
+        lib.ssk_volume_refresh.restype = i32
+        lib.ssk_volume_refresh.argtypes = [pV, ctypes.POINTER(vp), ctypes.POINTER(vp), i32, i32, i64, vp]
+        lib.ssk_volume_workspace_bytes.restype = sz
+        lib.ssk_volume_workspace_bytes.argtypes = [pV, pW]
+        lib.ssk_volume_ssim.restype = i32
+        lib.ssk_volume_ssim.argtypes = [pV, pW, i32, vp, vp, vp, sz, vp]
         lib.ssk_launch_count.restype = ctypes.c_uint64
         lib.ssk_probe_fp32_tflops.restype = i32
         lib.ssk_probe_fp32_tflops.argtypes = [ctypes.c_double, ctypes.POINTER(ctypes.c_double), vp]

@@ -85,7 +85,10 @@ __device__ __forceinline__ T load_sample(const unsigned char* p) {
 // Integer kernel: TIN in {u8, u16, u32}, ACC in {u32, u64}.
 // Grid: (strips, segments, frames); block = 128 threads = 128 input columns.
 // ---------------------------------------------------------------------------
-template <typename TIN, typename ACC>
+// MOM = true: the five per-pixel moments come precomputed from int64 planes
+// (the rolling temporal sums of a RollingVolume, src/spatiotemporal.py:60-138)
+// instead of being formed from staged x / y samples; everything else is shared.
+template <typename TIN, typename ACC, bool MOM = false>
 __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_constant__ BoxArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double s_red[(BX_THREADS / 32) * 3];
@@ -114,6 +117,7 @@ __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_consta
   const unsigned char* base_y = a.dist + (long long)frame * a.frame_pitch_b;
 
   auto issue_stage = [&](int chunk, int buf) {
+    if constexpr (MOM) return;  // moment planes are read straight from HBM
     const int rbase = r0 + chunk * CH;
     const int total = 2 * CH * nch;
     for (int i = tid; i < total; i += BX_THREADS) {
@@ -161,13 +165,22 @@ __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_consta
     const int bfirst = bnext;
     int nemit = 0;
     for (int g = 0; g < urows; ++g) {
-      const ACC x = (ACC)load_sample<TIN>(sx + g * P);
-      const ACC y = (ACC)load_sample<TIN>(sy + g * P);
-      pre[0] += x;
-      pre[1] += y;
-      pre[2] += x * x;
-      pre[3] += y * y;
-      pre[4] += x * y;
+      if constexpr (MOM) {
+        const int row = r0 + ubase + g, colx = c0 + tid;
+        if (colx < a.w) {
+          const long long* mp = a.mom + (long long)row * a.mom_rp + colx;
+#pragma unroll
+          for (int m = 0; m < 5; ++m) pre[m] += (ACC)mp[m * a.mom_plane];
+        }
+      } else {
+        const ACC x = (ACC)load_sample<TIN>(sx + g * P);
+        const ACC y = (ACC)load_sample<TIN>(sy + g * P);
+        pre[0] += x;
+        pre[1] += y;
+        pre[2] += x * x;
+        pre[3] += y * y;
+        pre[4] += x * y;
+      }
       const int u1 = ubase + g + 1;
       if (u1 == emit_at) {
         ACC* vr = vrow + (size_t)nemit * 5 * VP + tid;
@@ -286,6 +299,16 @@ size_t box_smem_bytes(const BoxArgs& a, bool wide) {
 template <typename TIN, typename ACC>
 static int launch_int_t(const BoxArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   auto fn = box_int_kernel<TIN, ACC>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return SSK_E_CUDA;
+  fn<<<grid, BX_THREADS, smem, st>>>(a);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+}
+
+int launch_box_moments(const BoxArgs& a, dim3 grid, cudaStream_t st) {
+  auto fn = box_int_kernel<uint8_t, unsigned long long, true>;
+  const size_t smem = box_smem_bytes(a, true);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SSK_E_CUDA;
   fn<<<grid, BX_THREADS, smem, st>>>(a);

@@ -461,6 +461,109 @@ int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, const dou
   return launch_msssim_finalize(fa, st);
 }
 
+}  // extern "C"
+
+namespace {
+
+int plan_volume(const ssk_volume* v, const ssk_window* win, int want, Plan& pl) {
+  if (!v || !v->planes || !win || v->h < 1 || v->w < 1 || v->depth < 1 || v->pitch < v->w) return SSK_E_ARG;
+  if (win->shape != SSK_RECT) return SSK_E_SHAPE;
+  if (win->k < 1 || win->stride < 1) return SSK_E_ARG;
+  if (win->k > v->h || win->k > v->w) return SSK_E_WINDOW;
+  const int k = win->k, s = win->stride;
+  BoxArgs& a = pl.ba;
+  a = BoxArgs{};
+  a.n = 1;
+  a.h = v->h;
+  a.w = v->w;
+  a.k = k;
+  a.s = s;
+  a.esize = 1;
+  a.dtype = SSK_U8;
+  pl.gh = a.gh = grid_extent(v->h, k, s);
+  pl.gw = a.gw = grid_extent(v->w, k, s);
+  a.sscale1 = a.sscale2 = 1.0;
+  a.area = (double)k * (double)k * (double)v->depth;
+  int ex = 0;
+  a.area_pow2 = std::frexp(a.area, &ex) == 0.5 ? 1 : 0;
+  a.inv_area = 1.0 / a.area;
+  a.c1 = win->c1;
+  a.c2 = win->c2;
+  a.want = want;
+  a.map_plane = (long long)pl.gh * pl.gw;
+  a.map_frame = a.map_plane * ((want & SSK_MAP_STATS) ? 5 : 3);
+  a.mom = static_cast<const long long*>(v->planes);
+  a.mom_rp = v->pitch;
+  a.mom_plane = v->pitch * v->h;
+  if (!v->is_float && k <= BX_THREADS - 15) {
+    pl.box_int = true;
+    pl.wide = true;
+    a.na = (BX_THREADS - 15 - k) / s + 1;
+    const int nstrips = (pl.gw + a.na - 1) / a.na;
+    int vr = 32 / s;
+    vr = vr < 1 ? 1 : (vr > 8 ? 8 : vr);
+    a.ch = vr * s;
+    a.in_pitch = 16;  // no staging for moment planes
+    a.nslot = (k + s - 1) / s + 1;
+    int seg_anchors = (256 + s - 1) / s;
+    long long nseg = (pl.gh + seg_anchors - 1) / seg_anchors;
+    seg_anchors = (int)((pl.gh + nseg - 1) / nseg);
+    a.seg_anchors = seg_anchors;
+    nseg = (pl.gh + seg_anchors - 1) / seg_anchors;
+    pl.grid = dim3(nstrips, (unsigned)nseg, 1);
+    pl.nparts_per_frame = (size_t)nstrips * nseg;
+    return SSK_OK;
+  }
+  pl.box_int = false;
+  pl.block = dim3(32, 4);
+  pl.grid = dim3((pl.gw + 31) / 32, (pl.gh + 3) / 4, 1);
+  pl.nparts_per_frame = (size_t)pl.grid.x * pl.grid.y;
+  return SSK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ssk_volume_update(const ssk_volume* v, const void* new_ref, const void* new_dist, const void* old_ref,
+                      const void* old_dist, int dtype, int64_t src_row_pitch, int mode, void* stream) {
+  if (!v || !v->planes || !new_ref || !new_dist || mode < 0 || mode > 2) return SSK_E_ARG;
+  if (mode == 2 && (!old_ref || !old_dist)) return SSK_E_ARG;
+  if (src_row_pitch < v->w) return SSK_E_ARG;
+  return launch_volume_update(v->planes, v->is_float, v->pitch * v->h, v->pitch, new_ref, new_dist, old_ref,
+                              old_dist, dtype, src_row_pitch, v->h, v->w, mode, static_cast<cudaStream_t>(stream));
+}
+
+int ssk_volume_refresh(const ssk_volume* v, const void* const* refs, const void* const* dists, int count,
+                       int dtype, int64_t src_row_pitch, void* stream) {
+  if (!v || !v->planes || !v->is_float || !refs || !dists) return SSK_E_ARG;
+  return launch_volume_refresh(v->planes, v->pitch * v->h, v->pitch, refs, dists, count, dtype, src_row_pitch,
+                               v->h, v->w, static_cast<cudaStream_t>(stream));
+}
+
+size_t ssk_volume_workspace_bytes(const ssk_volume* v, const ssk_window* win) {
+  Plan pl;
+  if (plan_volume(v, win, SSK_WANT_Q | SSK_WANT_L | SSK_WANT_CS, pl)) return 0;
+  return partial_bytes(pl, 1);
+}
+
+int ssk_volume_ssim(const ssk_volume* v, const ssk_window* win, int want, double* d_sums, void* d_maps,
+                    void* d_workspace, size_t workspace_bytes, void* stream) {
+  Plan pl;
+  const int rc = plan_volume(v, win, want, pl);
+  if (rc) return rc;
+  if (!d_sums || ((want & (SSK_MAP_TERMS | SSK_MAP_STATS)) && !d_maps)) return SSK_E_ARG;
+  if (!d_workspace || workspace_bytes < partial_bytes(pl, 1)) return SSK_E_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* partials = static_cast<double*>(d_workspace);
+  pl.ba.partials = partials;
+  pl.ba.maps = static_cast<double*>(d_maps);
+  int e = pl.box_int ? launch_box_moments(pl.ba, pl.grid, st)
+                     : launch_volume_direct(pl.ba, static_cast<const double*>(v->planes), pl.grid, pl.block, st);
+  if (e) return e;
+  return launch_reduce_partials(partials, (int)pl.nparts_per_frame, 1, 3, 1.0, d_sums, 3, 0, 0, st);
+}
+
 uint64_t ssk_launch_count(void) { return g_launches.load(); }
 
 int ssk_probe_fp32_tflops(double seconds, double* tflops, void* stream) {

@@ -73,10 +73,20 @@ struct BoxArgs {
   double* maps;               // float64 [n][planes][gh][gw]
   long long map_plane, map_frame;
   long long* wsums;           // optional int64 [n][5][gh][gw]
+  const long long* mom;       // moment planes [5][h][mom_rp] (volume path), else null
+  long long mom_rp, mom_plane;
 };
 
 size_t box_smem_bytes(const BoxArgs& a, bool wide);
 int launch_box_int(const BoxArgs& a, dim3 grid, bool wide, cudaStream_t st);
+int launch_box_moments(const BoxArgs& a, dim3 grid, cudaStream_t st);
+int launch_volume_update(void* planes, int is_float, long long pp, long long prp, const void* nr, const void* nd,
+                         const void* orf, const void* od, int dtype, long long srp, int h, int w, int mode,
+                         cudaStream_t st);
+int launch_volume_refresh(void* planes, long long pp, long long prp, const void* const* refs,
+                          const void* const* dists, int count, int dtype, long long srp, int h, int w,
+                          cudaStream_t st);
+int launch_volume_direct(const BoxArgs& a, const double* planes, dim3 grid, dim3 block, cudaStream_t st);
 int launch_box_float(const BoxArgs& a, dim3 grid, dim3 block, cudaStream_t st);
 bool box_block_supported(int dtype, int k, int s, bool wide, double stored_max);
 int launch_box_block(const BoxArgs& a, dim3 grid, cudaStream_t st);

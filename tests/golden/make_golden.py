@@ -145,6 +145,40 @@ def main() -> None:
     out["config1/sha256"] = np.frombuffer(hashlib.sha256(a.tobytes() + b.tobytes()).digest(), dtype=np.uint8)
     out["config1/terms"] = np.array([maps.q_map.values.mean(), maps.l_map.values.mean(), maps.cs_map.values.mean()])
 
+    # SSIM-3D rolling volumes (src/spatiotemporal.py): integer and float streams,
+    # a refresh inside the float run, and the multiscale variant
+    from ssimkit.spatiotemporal import RollingVolume, msssim3d, ssim3d_map, ssim3d_series
+
+    frames_a = [natural(rng, 36, 44) for _ in range(7)]
+    frames_b = [noisy(rng, f, 15, 255) for f in frames_a]
+    for i in range(7):
+        out[f"vol/ref{i}"], out[f"vol/dist{i}"] = frames_a[i], frames_b[i]
+    out["vol/series_k3"] = ssim3d_series([LumaPlane(f) for f in frames_a], [LumaPlane(f) for f in frames_b], 3,
+                                         SsimConfig(window=WindowSpec.rectangular(7))).scores
+    out["vol/series_k1"] = ssim3d_series([LumaPlane(f) for f in frames_a], [LumaPlane(f) for f in frames_b], 1,
+                                         SsimConfig(window=WindowSpec.rectangular(5, stride=2))).scores
+    vol = RollingVolume(4)
+    for fa, fb in zip(frames_a, frames_b):
+        vol.push(LumaPlane(fa), LumaPlane(fb))
+    st = vol.local_statistics(WindowSpec.rectangular(6))
+    out["vol/stats_k4_w6"] = np.stack([st.mu1, st.mu2, st.var1, st.var2, st.cov])
+    maps = ssim3d_map(vol, WindowSpec.rectangular(6), SsimConfig())
+    out["vol/q_k4_w6"] = maps.q_map.values
+    fl_a = [f.astype(np.float64) / 3.0 for f in frames_a]
+    fl_b = [f.astype(np.float64) / 3.0 for f in frames_b]
+    volf = RollingVolume(3, refresh_interval=4)
+    series = []
+    for fa, fb in zip(fl_a, fl_b):
+        volf.push(fa, fb)
+        series.append(float(ssim3d_map(volf, WindowSpec.rectangular(5)).q_map.values.mean()))
+    out["vol/series_float_refresh4"] = np.array(series)
+    big_a = [natural(rng, 48, 52) for _ in range(4)]
+    big_b = [noisy(rng, f, 20, 255) for f in big_a]
+    for i in range(4):
+        out[f"vol/msref{i}"], out[f"vol/msdist{i}"] = big_a[i], big_b[i]
+    out["vol/ms3d"] = msssim3d([LumaPlane(f) for f in big_a], [LumaPlane(f) for f in big_b], 2,
+                               MultiscaleSpec.product(3), SsimConfig(window=WindowSpec.rectangular(5))).scores
+
     np.savez_compressed(HERE / "golden_v1.npz", **out)
     print(f"wrote {len(out)} arrays, reference ssimkit {ssimkit.__version__}")
 

@@ -407,3 +407,89 @@ def test_sequence_scorer_multiscale_and_temporal_pooler(cuda, oracle, rng):
     assert np.max(np.abs(res.scores - want)) < 1e-12
     assert abs(res.pooled - P.pool_temporal(want, "hm")) < 1e-12
     assert all(r.am is None for r in res.records)
+
+
+# --- SSIM-3D rolling volumes (src/spatiotemporal.py) ----------------------------
+
+def test_ssim3d_against_golden(cuda, golden):
+    fa = [golden[f"vol/ref{i}"] for i in range(7)]
+    fb = [golden[f"vol/dist{i}"] for i in range(7)]
+    got = P.ssim3d_series(fa, fb, 3, P.SsimConfig(window=P.WindowSpec.rectangular(7))).scores
+    assert np.max(np.abs(got - golden["vol/series_k3"])) < 1e-12
+    got = P.ssim3d_series(fa, fb, 1, P.SsimConfig(window=P.WindowSpec.rectangular(5, stride=2))).scores
+    assert np.max(np.abs(got - golden["vol/series_k1"])) < 1e-12
+    vol = P.RollingVolume(4)
+    for a, b in zip(fa, fb):
+        P.push_frame(vol, P.LumaPlane(a), P.LumaPlane(b))
+    assert vol.depth == 4
+    st = vol.local_statistics(P.WindowSpec.rectangular(6))
+    assert np.array_equal(np.stack([st.mu1, st.mu2, st.var1, st.var2, st.cov]), golden["vol/stats_k4_w6"])
+    q = P.ssim3d_map(vol, P.WindowSpec.rectangular(6)).q_map.values
+    assert np.array_equal(q, golden["vol/q_k4_w6"])  # exact integer sums + reference fp64 epilogue
+    sums = vol.temporal_sums()
+    direct = vol.direct_sums()
+    assert all(np.array_equal(x, y) for x, y in zip(sums, direct))
+    ma = [golden[f"vol/msref{i}"] for i in range(4)]
+    mb = [golden[f"vol/msdist{i}"] for i in range(4)]
+    got = P.msssim3d(ma, mb, 2, P.MultiscaleSpec.product(3), P.SsimConfig(window=P.WindowSpec.rectangular(5))).scores
+    assert np.max(np.abs(got - golden["vol/ms3d"])) < 1e-12
+
+
+def test_ssim3d_float_refresh_against_golden(cuda, golden):
+    fa = [golden[f"vol/ref{i}"].astype(np.float64) / 3.0 for i in range(7)]
+    fb = [golden[f"vol/dist{i}"].astype(np.float64) / 3.0 for i in range(7)]
+    vol = P.RollingVolume(3, refresh_interval=4)
+    got = []
+    for a, b in zip(fa, fb):
+        vol.push(a, b)
+        got.append(float(P.ssim3d_map(vol, P.WindowSpec.rectangular(5)).q_map.values.mean()))
+    assert np.max(np.abs(np.array(got) - golden["vol/series_float_refresh4"])) < 1e-10
+
+
+def test_ssim3d_kt1_equals_framewise_and_errors(cuda, rng):
+    frames = [(rng.integers(0, 256, (40, 50)).astype(np.uint8), rng.integers(0, 256, (40, 50)).astype(np.uint8))
+              for _ in range(3)]
+    cfg = P.SsimConfig(window=P.WindowSpec.rectangular(7))
+    s3 = P.ssim3d_series([a for a, _ in frames], [b for _, b in frames], 1, cfg).scores
+    s2 = np.array([P.ssim_score(a, b, cfg) for a, b in frames])
+    assert np.max(np.abs(s3 - s2)) < 1e-12
+    vol = P.RollingVolume(2)
+    with pytest.raises(ValidationError):
+        vol.local_statistics(P.WindowSpec.rectangular(3))  # nothing buffered
+    vol.push(*frames[0])
+    from paper_2101_06354_b200.errors import GaussianNotSupported3D
+
+    with pytest.raises(GaussianNotSupported3D):
+        vol.local_statistics(P.WindowSpec.gaussian(1.5))
+    with pytest.raises(ValidationError):
+        vol.local_statistics(P.WindowSpec.rectangular(45))
+    with pytest.raises(DimensionMismatch):
+        vol.push(frames[0][0][:30], frames[0][1][:30])
+    with pytest.raises(ValidationError):
+        P.RollingVolume(0)
+
+
+def test_ssim3d_cost_independent_of_kt(cuda, rng):
+    """Acceptance criterion C4 (tests/test_acceptance.py:120-160): per-frame cost ~ independent of Kt."""
+    import time
+
+    import torch
+
+    frames = [(rng.integers(0, 256, (256, 256)).astype(np.uint8), rng.integers(0, 256, (256, 256)).astype(np.uint8))
+              for _ in range(24)]
+    cfg = P.SsimConfig(window=P.WindowSpec.rectangular(8))
+
+    def run(kt):
+        vol = P.RollingVolume(kt)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for a, b in frames:
+            vol.push(a, b)
+            vol.terms(cfg.window, cfg)
+        torch.cuda.synchronize()
+        return time.perf_counter() - t0
+
+    run(2)
+    t2 = min(run(2) for _ in range(2))
+    t10 = min(run(10) for _ in range(2))
+    assert t10 / t2 < 1.5

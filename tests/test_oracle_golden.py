@@ -116,3 +116,22 @@ def test_grid_shape_formula(oracle, rng):
     for k, s in [(5, 1), (5, 3), (8, 4), (11, 5)]:
         mu1 = oracle.local_statistics(a, a, "rect", k, s)[0]
         assert mu1.shape == ((37 - k) // s + 1, (23 - k) // s + 1)
+
+
+def test_ssim3d_oracle_against_golden(golden, oracle):
+    fa = [golden[f"vol/ref{i}"] for i in range(7)]
+    fb = [golden[f"vol/dist{i}"] for i in range(7)]
+    assert oracle.ssim3d_series(fa, fb, 3, k=7) == list(golden["vol/series_k3"])
+    assert oracle.ssim3d_series(fa, fb, 1, k=5, stride=2) == list(golden["vol/series_k1"])
+    vol = oracle.RollingSums(4)
+    for a, b in zip(fa, fb):
+        vol.push(a, b)
+    assert np.array_equal(np.stack(vol.stats(6)), golden["vol/stats_k4_w6"])
+    c1, c2 = oracle.constants(8)
+    assert np.array_equal(oracle.term_maps(*vol.stats(6), c1, c2)[2], golden["vol/q_k4_w6"])
+    fl_a = [f.astype(np.float64) / 3.0 for f in fa]
+    fl_b = [f.astype(np.float64) / 3.0 for f in fb]
+    assert oracle.ssim3d_series(fl_a, fl_b, 3, k=5, refresh_interval=4) == list(golden["vol/series_float_refresh4"])
+    ma = [golden[f"vol/msref{i}"] for i in range(4)]
+    mb = [golden[f"vol/msdist{i}"] for i in range(4)]
+    assert oracle.msssim3d(ma, mb, 2, levels=3, k=5) == list(golden["vol/ms3d"])
