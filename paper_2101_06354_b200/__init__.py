@@ -59,7 +59,7 @@ from .scoring import (
     weber_contrast_term,
     weber_luminance_term,
 )
-from .video import SequenceScorer, gather_frame_scores, score_sequence, shard_bounds
+from .video import FrameScore, SequenceScorer, gather_frame_scores, score_frame_pair, score_sequence, shard_bounds
 from .volume import REFRESH_INTERVAL, RollingVolume, msssim3d, push_frame, ssim3d_map, ssim3d_series
 
 __version__ = "0.1.0"
@@ -85,7 +85,7 @@ __all__ = [
     "SpatialPooler", "TemporalPooler", "pool_spatial", "pool_temporal",
     # batched device API / sequences / multi-GPU
     "FrameTerms", "HostBatchScorer", "color_batch", "msssim_batch", "ssim_batch", "ssim_terms_batch",
-    "SequenceScorer", "gather_frame_scores", "score_sequence", "shard_bounds",
+    "SequenceScorer", "gather_frame_scores", "score_sequence", "shard_bounds", "FrameScore", "score_frame_pair",
     # spatio-temporal (SSIM-3D)
     "REFRESH_INTERVAL", "RollingVolume", "msssim3d", "push_frame", "ssim3d_map", "ssim3d_series",
 ]

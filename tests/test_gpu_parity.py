@@ -493,3 +493,36 @@ def test_ssim3d_cost_independent_of_kt(cuda, rng):
     t2 = min(run(2) for _ in range(2))
     t10 = min(run(10) for _ in range(2))
     assert t10 / t2 < 1.5
+
+
+def test_score_frame_pair_contract(cuda, oracle, rng, golden):
+    a = rng.integers(0, 256, (60, 72)).astype(np.uint8)
+    b = np.clip(a.astype(int) + rng.integers(-25, 26, a.shape), 0, 255).astype(np.uint8)
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    rec = P.score_frame_pair(P.LumaPlane(a), P.LumaPlane(b), cfg)
+    want = oracle.ssim_terms(a, b, shape="gauss", k=11, sigma=1.5)
+    assert abs(rec.score - want[0]) < 1e-5 and rec.am == rec.score
+    assert abs(rec.l_mean - want[1]) < 1e-5 and abs(rec.cs_mean - want[2]) < 1e-5
+    # non-mean spatial pooling pools the device map (and mean-luma map for lw)
+    cfg_cov = P.SsimConfig(spatial_pool="cov")
+    rec = P.score_frame_pair(a, b, cfg_cov)
+    l_map, cs_map, q = oracle.ssim_maps(a, b)
+    assert abs(rec.score - float(q.std() / q.mean())) < 1e-12
+    mu1 = oracle.local_statistics(a, b, "rect", 11)[0]
+    rec = P.score_frame_pair(a, b, P.SsimConfig(spatial_pool="lw:a=100,b=50"))
+    wts = np.clip((mu1 - 100) / 50, 0, 1)
+    assert abs(rec.score - float((wts * q).mean())) < 1e-12
+    ms = P.score_frame_pair(a, b, P.SsimConfig(window=P.WindowSpec.rectangular(5), multiscale=P.MultiscaleSpec.product(3)))
+    assert abs(ms.score - oracle.msssim(a, b, 3, shape="rect", k=5)) < 1e-12 and ms.am is None
+    ref = P.ColorFrame(tuple(golden[f"color/ref{i}"] for i in range(3)), "ycbcr-bt709", "420")
+    dist = P.ColorFrame(tuple(golden[f"color/dist{i}"] for i in range(3)), "ycbcr-bt709", "420")
+    fx = P.score_frame_pair(ref, dist, P.SsimConfig(window=P.WindowSpec.gaussian(1.5),
+                                                    color=P.ColorModelSpec("fixed", weights=(4 / 6, 1 / 6, 1 / 6))))
+    assert abs(fx.score - float(golden["color/fixed"])) < 1e-5
+    vol = P.RollingVolume(2)
+    r3 = P.score_frame_pair(a, b, P.SsimConfig(window=P.WindowSpec.rectangular(7)), volume=vol)
+    assert abs(r3.score - oracle.ssim_score(a, b, shape="rect", k=7)) < 1e-12
+    with pytest.raises(ValidationError):
+        P.score_frame_pair(a, b, P.SsimConfig(color=P.ColorModelSpec("qssim")))
+    with pytest.raises(ValidationError):
+        P.score_frame_pair(a, b, P.SsimConfig(scaling=P.ScalePolicy.legacy256()))
