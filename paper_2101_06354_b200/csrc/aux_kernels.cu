@@ -295,32 +295,53 @@ __global__ void __launch_bounds__(128) pyramid_kernel(const __grid_constant__ Py
   // level-1 rows of the block, kept in registers for the coarser levels
   TA lv[B / 2][B / 2];
   const bool full = (r0 + B <= 2 * p.hl[0]) && (c0 + B <= 2 * p.wl[0]);
+  constexpr bool VEC = (B * sizeof(TS)) % 16 == 0 && B * sizeof(TS) <= 16;  // one 16-B vector per row
+  if (VEC && full) {
+    // interior block: issue all B row loads before any arithmetic (memory-level parallelism)
+    uint4 rows[B];
 #pragma unroll
-  for (int i = 0; i < B / 2; ++i) {
-    TS a0[B], a1[B];
-    const TS* s0 = src + (long long)(r0 + 2 * i) * p.src_rp + c0;
-    const TS* s1 = s0 + p.src_rp;
-    if (full && (B * sizeof(TS)) % 16 == 0) {
+    for (int r = 0; r < B; ++r) rows[r] = *reinterpret_cast<const uint4*>(src + (long long)(r0 + r) * p.src_rp + c0);
 #pragma unroll
-      for (int v = 0; v < (int)(B * sizeof(TS) / 16); ++v) {
-        reinterpret_cast<uint4*>(a0)[v] = reinterpret_cast<const uint4*>(s0)[v];
-        reinterpret_cast<uint4*>(a1)[v] = reinterpret_cast<const uint4*>(s1)[v];
-      }
-    } else {
-      const bool rok = r0 + 2 * i + 1 < 2 * p.hl[0] + 1 && r0 + 2 * i < 2 * p.hl[0];
+    for (int i = 0; i < B / 2; ++i) {
+      const TS* a0 = reinterpret_cast<const TS*>(&rows[2 * i]);
+      const TS* a1 = reinterpret_cast<const TS*>(&rows[2 * i + 1]);
 #pragma unroll
-      for (int j = 0; j < B; ++j) {
-        const bool ok = rok && c0 + j < 2 * p.wl[0];
-        a0[j] = ok ? s0[j] : (TS)0;
-        a1[j] = ok ? s1[j] : (TS)0;
+      for (int j = 0; j < B / 2; ++j) {
+        if constexpr (FLT) {
+          lv[i][j] = (((a0[2 * j] + a0[2 * j + 1]) + a1[2 * j]) + a1[2 * j + 1]) / (TS)4;
+        } else {
+          lv[i][j] = (TA)a0[2 * j] + a0[2 * j + 1] + a1[2 * j] + a1[2 * j + 1];
+        }
       }
     }
+  } else {
 #pragma unroll
-    for (int j = 0; j < B / 2; ++j) {
-      if constexpr (FLT) {
-        lv[i][j] = (((a0[2 * j] + a0[2 * j + 1]) + a1[2 * j]) + a1[2 * j + 1]) / (TS)4;
+    for (int i = 0; i < B / 2; ++i) {
+      TS a0[B], a1[B];
+      const TS* s0 = src + (long long)(r0 + 2 * i) * p.src_rp + c0;
+      const TS* s1 = s0 + p.src_rp;
+      if (full && (B * sizeof(TS)) % 16 == 0) {
+#pragma unroll
+        for (int v = 0; v < (int)(B * sizeof(TS) / 16); ++v) {
+          reinterpret_cast<uint4*>(a0)[v] = reinterpret_cast<const uint4*>(s0)[v];
+          reinterpret_cast<uint4*>(a1)[v] = reinterpret_cast<const uint4*>(s1)[v];
+        }
       } else {
-        lv[i][j] = (TA)a0[2 * j] + a0[2 * j + 1] + a1[2 * j] + a1[2 * j + 1];
+        const bool rok = r0 + 2 * i < 2 * p.hl[0];
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+          const bool ok = rok && c0 + j < 2 * p.wl[0];
+          a0[j] = ok ? s0[j] : (TS)0;
+          a1[j] = ok ? s1[j] : (TS)0;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < B / 2; ++j) {
+        if constexpr (FLT) {
+          lv[i][j] = (((a0[2 * j] + a0[2 * j + 1]) + a1[2 * j]) + a1[2 * j + 1]) / (TS)4;
+        } else {
+          lv[i][j] = (TA)a0[2 * j] + a0[2 * j + 1] + a1[2 * j] + a1[2 * j + 1];
+        }
       }
     }
   }

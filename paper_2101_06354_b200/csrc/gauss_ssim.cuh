@@ -219,6 +219,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
   const bool want_maps = (a.want & (SSK_MAP_TERMS | SSK_MAP_STATS)) != 0;
   const int s = a.stride;
   const int wo = a.wo;
+  const bool exact_sq = a.exact_sq != 0;
 
   double tq0 = 0.0, tl0 = 0.0, tc0 = 0.0, tq1 = 0.0, tl1 = 0.0, tc1 = 0.0;
   const int htid = WS ? tid - GS_THREADS : tid;
@@ -244,9 +245,11 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
         P[0] = X;
         P[1] = Y;
         if constexpr (NM == 4) {
-          // x'^2 and y'^2 are exact for 8-bit samples (|x'| <= 128), so the contracted
-          // x'^2 + y'^2 is still exactly symmetric; otherwise use IEEE scalar ops
+          // x'^2 and y'^2 are exact in fp32 for 8-bit samples (|x'| <= 128) and for the
+          // first two pyramid levels of 8-bit input (quarter / sixteenth steps), so the
+          // contracted x'^2 + y'^2 is still exactly symmetric there; otherwise IEEE scalar ops
           if constexpr (sizeof(TIN) == 1) P[2] = fma2(X, X, mul2(Y, Y));
+          else if (exact_sq) P[2] = fma2(X, X, mul2(Y, Y));
           else P[2] = sumsq2(X, Y);
           P[3] = mul2(X, Y);
         } else {

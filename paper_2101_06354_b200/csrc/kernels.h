@@ -23,6 +23,7 @@ struct GaussArgs {
   float shift;                // added back to the means
   float c1, c2;
   int want;
+  int exact_sq;               // shifted samples square exactly in fp32 (symmetric fast products)
   float taps[32];
   double* partials;           // [n][gridDim.y][gridDim.x][3]; gridDim.z = ceil(n / 2) frame pairs
   void* maps;                 // float32 [n][planes][gh][gw]
