@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SSK_ABI_VERSION 3
+#define SSK_ABI_VERSION 4
 
 /* sample storage types */
 enum {
@@ -166,11 +166,12 @@ int ssk_downsample(const ssk_planes* src, void* d_dst_ref, void* d_dst_dist, int
  *                 of max(s, 0)^e, 2 = sum of e*s, with `exponents` (host array,
  *                 `levels` entries, already renormalised for sum/fast4 as
  *                 MultiscaleSpec.effective_exponents does); aggregation 0 = none;
- *   d_ssim_sums   [n][3] (nullable): level-0 (sum q, sum l, sum cs) -- the plain
- *                 SSIM of the same pass (scale 0 is shared).
+ *   d_ssim_means  [n][3] (nullable): level-0 (mean q, mean l, mean cs) -- the
+ *                 plain SSIM record (score, l_mean, cs_mean) of the same pass
+ *                 (scale 0 is shared).
  */
 int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, const double* exponents,
-               int aggregation, double* d_level_means, double* d_scores, double* d_ssim_sums,
+               int aggregation, double* d_level_means, double* d_scores, double* d_ssim_means,
                void* d_workspace, size_t workspace_bytes, void* stream);
 
 /*

@@ -82,9 +82,7 @@ def msssim_batch(ref, dist, config: SsimConfig = SsimConfig(), spec: Optional[Mu
                                                with_ssim=with_ssim, spec=spec, stream=stream)
     if not with_ssim:
         return score
-    gh, gw = engine.grid_shape(h, w, k, config.window.stride)
-    m = engine.frame_means(ssim_sums, gh * gw)
-    return score, FrameTerms(m[:, 0], m[:, 1], m[:, 2])
+    return score, FrameTerms(ssim_sums[:, 0], ssim_sums[:, 1], ssim_sums[:, 2])
 
 
 def color_batch(planes_ref, planes_dist, config: SsimConfig = SsimConfig(), weights=None,

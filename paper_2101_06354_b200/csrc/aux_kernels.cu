@@ -450,7 +450,7 @@ __global__ void msssim_finalize_kernel(const __grid_constant__ FinalizeArgs a) {
         double t = 0.0;
         for (int i = lane; i < a.nparts[0]; i += 32) t += p[(long long)i * 3 + c];
         t = warp_sum(t);
-        if (lane == 0) a.ssim_sums[(long long)f * 3 + c] = t;
+        if (lane == 0) a.ssim_sums[(long long)f * 3 + c] = __ddiv_rn(t, a.count[0]);
       }
     }
     if (lane == 0) {

@@ -367,7 +367,7 @@ size_t ssk_msssim_workspace_bytes(const ssk_planes* p, const ssk_window* win, in
 }
 
 int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, const double* exponents,
-               int aggregation, double* d_level_means, double* d_scores, double* d_ssim_sums,
+               int aggregation, double* d_level_means, double* d_scores, double* d_ssim_means,
                void* d_workspace, size_t workspace_bytes, void* stream) {
   int rc = check_planes(p);
   if (rc) return rc;
@@ -418,14 +418,14 @@ int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, const dou
   fa.aggregation = aggregation;
   fa.level_means = d_level_means;
   fa.scores = d_scores;
-  fa.ssim_sums = d_ssim_sums;
+  fa.ssim_sums = d_ssim_means;
   for (int l = 0; l < levels; ++l) fa.exps[l] = aggregation ? exponents[l] : 0.0;
   size_t part_off = pyr;
   Plan plans[16];
   for (int l = 0; l < levels; ++l) {
     const bool last = l == levels - 1;
     int want = last ? SSK_WANT_Q : SSK_WANT_CS;
-    if (l == 0 && d_ssim_sums) want |= SSK_WANT_Q | SSK_WANT_L | SSK_WANT_CS;
+    if (l == 0 && d_ssim_means) want |= SSK_WANT_Q | SSK_WANT_L | SSK_WANT_CS;
     rc = plan_ssim(&lv[l].planes, win, want, plans[l]);
     if (rc) return rc;
     fa.partials[l] = reinterpret_cast<const double*>(ws + part_off);

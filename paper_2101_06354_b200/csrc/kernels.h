@@ -114,7 +114,7 @@ struct FinalizeArgs {
   int aggregation;        // 0: level means only, 1: product, 2: sum
   double* level_means;    // [n][levels]
   double* scores;         // [n] or null
-  double* ssim_sums;      // [n][3] or null (level-0 sums of q, l, cs)
+  double* ssim_sums;      // [n][3] or null: level-0 means of q, l, cs (sum / count, IEEE division)
 };
 int launch_msssim_finalize(const FinalizeArgs& a, cudaStream_t st);
 

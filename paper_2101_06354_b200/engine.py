@@ -181,7 +181,8 @@ def msssim_levels(pair: DevicePair, window, c1: float, c2: float, levels: int,
     """Whole MS-SSIM pyramid in one library call.
 
     Returns (level means [n, levels] (cs below the coarsest, q at it), combined
-    score [n] or None (when ``spec`` is given), level-0 SSIM sums [n, 3] or None).
+    score [n] or None (when ``spec`` is given), level-0 SSIM means (q, l, cs)
+    [n, 3] or None).
     """
     torch = nat.torch_mod()
     lib = nat.lib()
