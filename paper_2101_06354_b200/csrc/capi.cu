@@ -11,6 +11,11 @@
 
 namespace ssk {
 namespace gk {
+int gauss_ws_level();
+}
+}  // namespace ssk
+namespace ssk {
+namespace gk {
 int gauss_ws_level() {
   static const int v = [] {
     const char* e = std::getenv("SSK_GAUSS_WS");  // warp-specialised K1 (default on; 0 = classic)
@@ -96,7 +101,11 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
     a.gh = pl.gh;
     a.gw = pl.gw;
     a.stride = s;
-    const int nstrips = (a.wo + gauss_tw(k) - 1) / gauss_tw(k);
+    // wide strips (256 V columns, 1 CTA/SM) for 8-bit frames under the warp-specialised
+    // kernel: V-halo overhead 250/240 instead of 122/112 and fewer idle H threads
+    a.vcols = (gk::gauss_ws_level() >= 1 && p->dtype == SSK_U8 && k <= 17 && a.wo >= 480) ? 256 : 128;
+    const int tw = gauss_tw(k, a.vcols);
+    const int nstrips = (a.wo + tw - 1) / tw;
     // Segments depend on the frame geometry only (never on the batch size), so a
     // frame's fp32 partial sums -- and hence its score -- are bit-identical
     // however frames are batched or sharded.

@@ -102,9 +102,10 @@ inline bool gauss_ws_enabled() { return gauss_ws_level() >= 1; }
 #ifndef GS_MINB
 #define GS_MINB (NM == 4 ? 4 : 3)  // 4 CTAs/SM measured faster than 3 with more registers
 #endif
-constexpr int VP = GS_VCOLS * 8 + 8;          // V-row pitch (bytes): a half warp's 8 rows x 2 column groups hit distinct banks
-
-__host__ __device__ constexpr int tw_of(int k) { return ((GS_VCOLS - (k - 1)) / 16) * 16; }
+// V-row pitch in bytes for VC columns: pitch/8 odd -> a half warp's 8 rows x 2 column
+// groups hit 16 distinct 8-byte bank slots
+__host__ __device__ constexpr int vp_of(int vc) { return vc * 8 + 8; }
+__host__ __device__ constexpr int tw_of(int k, int vc) { return ((vc - (k - 1)) / 16) * 16; }
 
 // raw sample (as stored) -> float with the 2^23 splice for small integers
 template <typename TIN>
@@ -145,10 +146,11 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-template <int K, typename TIN, int NM, bool WS>
+template <int K, typename TIN, int NM, bool WS, int VC>
 __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, const int seg, const int pair,
                                            const int nstrips, const int nseg) {
-  constexpr int TW = tw_of(K);
+  constexpr int VP = vp_of(VC);
+  constexpr int TW = tw_of(K, VC);
   constexpr int TWI = TW + K - 1;
   constexpr int ES = (int)sizeof(TIN);
   constexpr int RB = ((TWI * ES + 15) / 16) * 16;  // raw row bytes per image
@@ -156,14 +158,14 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
   constexpr int RR = 2 * G + K - 1;                 // raw ring rows
   constexpr int NH = (K + 1) / 2;
   constexpr int NP = 8 + K - 1;                     // V values read per H item
-  static_assert(TWI <= GS_THREADS, "strip wider than the CTA");
+  static_assert(TWI <= VC, "strip wider than the CTA");
 
-  constexpr int NT = WS ? 2 * GS_THREADS : GS_THREADS;  // threads per CTA
+  constexpr int NT = WS ? 2 * VC : VC;  // threads per CTA
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* raw = smem;                        // [RR][4][RB]
   unsigned char* vbuf0 = smem + RR * 4 * RB;        // [WS ? 2 : 1][NM][G][VP]
   __shared__ float s_taps[32];
-  __shared__ double s_red[(2 * GS_THREADS / 32) * 6];
+  __shared__ double s_red[(2 * VC / 32) * 6];
 
   const int tid = threadIdx.x;
   const int f0 = 2 * pair;
@@ -179,10 +181,10 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
   const long long fo0 = (long long)f0 * a.frame_pitch_b, fo1 = (long long)f1 * a.frame_pitch_b;
   const int row_bytes_left = (a.w - c0) * ES;
 
-  auto stage_rows = [&](int r_lo, int r_hi) {  // issued by the GS_THREADS V-pass threads
+  auto stage_rows = [&](int r_lo, int r_hi) {  // issued by the VC V-pass threads
     r_hi = min(r_hi, in_end);
     const int total = (r_hi - r_lo) * 4 * NCH;
-    for (int i = tid; i < total; i += GS_THREADS) {
+    for (int i = tid; i < total; i += VC) {
       const int rr = i / (4 * NCH);
       const int rem = i - rr * (4 * NCH);
       const int im = rem / NCH;
@@ -200,7 +202,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
     cp_async_commit();
   };
 
-  if (tid < GS_THREADS) stage_rows(y0, y0 + G + K - 1);
+  if (tid < VC) stage_rows(y0, y0 + G + K - 1);
   if (tid < 32) s_taps[tid] = a.taps[tid];
   __syncthreads();
   u64 w2[NH];
@@ -222,7 +224,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
   const bool exact_sq = a.exact_sq != 0;
 
   double tq0 = 0.0, tl0 = 0.0, tc0 = 0.0, tq1 = 0.0, tl1 = 0.0, tc1 = 0.0;
-  const int htid = WS ? tid - GS_THREADS : tid;
+  const int htid = WS ? tid - VC : tid;
   const int hg = htid % G, hj = htid / G;  // H item: output row hg of the chunk, columns 8*hj..8*hj+7
 
   // ---------------- V pass: thread = input column ----------------
@@ -397,7 +399,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
     constexpr int VBYTES = NM * G * VP;
     // GS_NBUF V tiles in flight; named barriers 2..2+NBUF-1 = "tile b full",
     // 2+NBUF.. = "tile b free"; barrier 1 = producer-internal
-    if (tid < GS_THREADS) {  // producers
+    if (tid < VC) {  // producers
       int b = 0;
       for (int c = 0; c < nchunks; ++c) {
         if (c + 1 < nchunks) {
@@ -406,19 +408,19 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
         } else {
           cp_async_wait<0>();
         }
-        named_sync(1, GS_THREADS);                                   // chunk c's raw rows visible
-        if (c >= GS_NBUF) named_sync(2 + GS_NBUF + b, 2 * GS_THREADS);  // consumers released tile b
+        named_sync(1, VC);                                           // chunk c's raw rows visible
+        if (c >= GS_NBUF) named_sync(2 + GS_NBUF + b, 2 * VC);       // consumers released tile b
         vpass(c, vbuf0 + b * VBYTES);
-        named_arrive(2 + b, 2 * GS_THREADS);                         // tile b full
-        named_sync(1, GS_THREADS);                                   // raw rows of chunk c no longer read
+        named_arrive(2 + b, 2 * VC);                                 // tile b full
+        named_sync(1, VC);                                           // raw rows of chunk c no longer read
         b = b + 1 == GS_NBUF ? 0 : b + 1;
       }
     } else {  // consumers
       int b = 0;
       for (int c = 0; c < nchunks; ++c) {
-        named_sync(2 + b, 2 * GS_THREADS);
+        named_sync(2 + b, 2 * VC);
         hpass(c, vbuf0 + b * VBYTES);
-        if (c + GS_NBUF < nchunks) named_arrive(2 + GS_NBUF + b, 2 * GS_THREADS);
+        if (c + GS_NBUF < nchunks) named_arrive(2 + GS_NBUF + b, 2 * VC);
         b = b + 1 == GS_NBUF ? 0 : b + 1;
       }
     }
@@ -444,12 +446,12 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
 
 template <int K, typename TIN, int NM>
 __global__ void __launch_bounds__(GS_THREADS, GS_MINB) gauss_pair_kernel(const __grid_constant__ GaussArgs a) {
-  gauss_body<K, TIN, NM, false>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.x, gridDim.y);
+  gauss_body<K, TIN, NM, false, GS_THREADS>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.x, gridDim.y);
 }
 
-template <int K, typename TIN, int NM>
-__global__ void __launch_bounds__(2 * GS_THREADS, 2) gauss_ws_kernel(const __grid_constant__ GaussArgs a) {
-  gauss_body<K, TIN, NM, true>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.x, gridDim.y);
+template <int K, typename TIN, int NM, int VC>
+__global__ void __launch_bounds__(2 * VC, VC == 128 ? 2 : 1) gauss_ws_kernel(const __grid_constant__ GaussArgs a) {
+  gauss_body<K, TIN, NM, true, VC>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.x, gridDim.y);
 }
 
 // All pyramid levels of one sample type in one launch: blockIdx.x enumerates the
@@ -464,30 +466,34 @@ __global__ void __launch_bounds__(WS ? 2 * GS_THREADS : GS_THREADS, WS ? 2 : 4)
     if (i < p.nlev && (int)blockIdx.x >= p.cta_off[i]) lv = i;
   const int local = blockIdx.x - p.cta_off[lv];
   const int ns = p.nstrips[lv];
-  gauss_body<K, TIN, NM, WS>(p.lv[lv], local % ns, local / ns, blockIdx.z, ns, p.nseg[lv]);
+  gauss_body<K, TIN, NM, WS, GS_THREADS>(p.lv[lv], local % ns, local / ns, blockIdx.z, ns, p.nseg[lv]);
 }
 
-template <int K, typename TIN, int NM>
+template <int K, typename TIN, int NM, int VC = GS_THREADS>
 inline size_t smem_bytes() {
-  constexpr int TWI = tw_of(K) + K - 1;
+  constexpr int TWI = tw_of(K, VC) + K - 1;
   constexpr int RB = ((TWI * (int)sizeof(TIN) + 15) / 16) * 16;
-  return (size_t)(2 * G + K - 1) * 4 * RB + (size_t)NM * G * VP;
+  return (size_t)(2 * G + K - 1) * 4 * RB + (size_t)NM * G * vp_of(VC);
 }
 
-template <int K, typename TIN, int NM>
+template <int K, typename TIN, int NM, int VC>
 int launch_ws(const GaussArgs& a, dim3 grid, cudaStream_t st) {
-  auto fn = gauss_ws_kernel<K, TIN, NM>;
-  const size_t smem = smem_bytes<K, TIN, NM>() + (size_t)(GS_NBUF - 1) * NM * G * VP;  // extra V tiles
+  auto fn = gauss_ws_kernel<K, TIN, NM, VC>;
+  const size_t smem = smem_bytes<K, TIN, NM, VC>() + (size_t)(GS_NBUF - 1) * NM * G * vp_of(VC);  // extra V tiles
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SSK_E_CUDA;
-  fn<<<grid, 2 * GS_THREADS, smem, st>>>(a);
+  fn<<<grid, 2 * VC, smem, st>>>(a);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
 }
 
 template <int K, typename TIN, int NM>
 int launch_nm(const GaussArgs& a, dim3 grid, cudaStream_t st) {
-  if (NM == 4 && gauss_ws_enabled()) return launch_ws<K, TIN, NM>(a, grid, st);
+  if (NM == 4 && a.vcols == 256) {
+    if constexpr (sizeof(TIN) == 1 && 256 - (K - 1) >= 16) return launch_ws<K, TIN, NM, 256>(a, grid, st);
+    return SSK_E_ARG;
+  }
+  if (NM == 4 && gauss_ws_enabled()) return launch_ws<K, TIN, NM, GS_THREADS>(a, grid, st);
   auto fn = gauss_pair_kernel<K, TIN, NM>;
   const size_t smem = smem_bytes<K, TIN, NM>();
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -509,7 +515,7 @@ int launch_levels_one(const GaussLevels& p, dim3 grid, cudaStream_t st) {
   // (small tiles, 3-4 CTAs/SM); SSK_GAUSS_WS=2 forces the warp-specialised variant
   const bool ws = gauss_ws_level() >= 2;
   auto fn = ws ? gauss_levels_kernel<K, TIN, 4, true> : gauss_levels_kernel<K, TIN, 4, false>;
-  const size_t smem = smem_bytes<K, TIN, 4>() + (ws ? (size_t)(GS_NBUF - 1) * 4 * G * VP : 0);
+  const size_t smem = smem_bytes<K, TIN, 4>() + (ws ? (size_t)(GS_NBUF - 1) * 4 * G * vp_of(GS_THREADS) : 0);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SSK_E_CUDA;
   fn<<<grid, ws ? 2 * GS_THREADS : GS_THREADS, smem, st>>>(p);

@@ -24,6 +24,7 @@ struct GaussArgs {
   float c1, c2;
   int want;
   int exact_sq;               // shifted samples square exactly in fp32 (symmetric fast products)
+  int vcols;                  // V-pass columns per CTA: 128, or 256 (wide warp-specialised u8 kernel)
   float taps[32];
   double* partials;           // [n][gridDim.y][gridDim.x][3]; gridDim.z = ceil(n / 2) frame pairs
   void* maps;                 // float32 [n][planes][gh][gw]
@@ -43,7 +44,8 @@ struct GaussLevels {
 
 int launch_gauss_levels(const GaussLevels& p, dim3 grid, int k, int dtype, cudaStream_t st);
 
-inline int gauss_tw(int k) { return ((GS_VCOLS - (k - 1)) / 16) * 16; }  // output columns per strip
+// output columns per strip for a V pass of vc columns (16-column aligned strips)
+inline int gauss_tw(int k, int vc = GS_VCOLS) { return ((vc - (k - 1)) / 16) * 16; }
 int launch_gauss(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 int launch_gauss_u8(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 int launch_gauss_u16(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
