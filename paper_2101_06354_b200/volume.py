@@ -64,11 +64,8 @@ class RollingVolume:
     def _upload(self, a: np.ndarray):
         torch = nat.torch_mod()
         dev = nat.require_device()
-        if self._is_float:
-            t = torch.as_tensor(np.asarray(a, dtype=np.float64), device=dev)
-        else:
-            t = torch.as_tensor(np.asarray(a, dtype=np.uint8 if self._code == nat.U8 else np.uint16), device=dev)
-        return t.contiguous()
+        dt = np.float64 if self._is_float else (np.uint8 if self._code == nat.U8 else np.uint16)
+        return torch.from_numpy(np.array(a, dtype=dt, copy=True, order="C")).to(dev)
 
     def push(self, ref: PlaneLike, dist: PlaneLike) -> "RollingVolume":
         """Advance the temporal window by one frame pair (src/spatiotemporal.py:60-97)."""
