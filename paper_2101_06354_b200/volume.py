@@ -77,7 +77,8 @@ class RollingVolume:
             ints = a.dtype.kind in "ui" and b.dtype.kind in "ui" and min(a.min(), b.min()) >= 0
             hi = max(int(a.max()), int(b.max())) if ints else 0
             self._is_float = not (ints and hi <= 0xFFFF)
-            self._code = nat.F64 if self._is_float else (nat.U8 if hi <= 255 else nat.U16)
+            small = a.dtype == np.uint8 and b.dtype == np.uint8
+            self._code = nat.F64 if self._is_float else (nat.U8 if small else nat.U16)
             h, w = self._dims
             dt = torch.float64 if self._is_float else torch.int64
             self._planes = torch.zeros((5, h, w), dtype=dt, device=nat.require_device())
