@@ -60,6 +60,7 @@ from .scoring import (
     weber_luminance_term,
 )
 from .video import FrameScore, SequenceScorer, gather_frame_scores, score_frame_pair, score_sequence, shard_bounds
+from .ingest import FrameSource, StreamHeader, open_raw, open_y4m, score_files, write_planar_raw, write_y4m
 from .volume import REFRESH_INTERVAL, RollingVolume, msssim3d, push_frame, ssim3d_map, ssim3d_series
 
 __version__ = "0.1.0"
@@ -86,6 +87,8 @@ __all__ = [
     # batched device API / sequences / multi-GPU
     "FrameTerms", "HostBatchScorer", "color_batch", "msssim_batch", "ssim_batch", "ssim_terms_batch",
     "SequenceScorer", "gather_frame_scores", "score_sequence", "shard_bounds", "FrameScore", "score_frame_pair",
+    # media ingest
+    "FrameSource", "StreamHeader", "open_raw", "open_y4m", "score_files", "write_planar_raw", "write_y4m",
     # spatio-temporal (SSIM-3D)
     "REFRESH_INTERVAL", "RollingVolume", "msssim3d", "push_frame", "ssim3d_map", "ssim3d_series",
 ]

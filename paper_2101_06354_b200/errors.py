@@ -87,3 +87,24 @@ class DegenerateData(SsimkitError):
 
 class EngineUnavailable(SsimkitError, RuntimeError):
     """The CUDA engine (libssimk.so on a B200) is missing: there is no CPU fallback."""
+
+
+# media ingest (src/errors.py, media section)
+class BadMagic(SsimkitError):
+    """Stream does not start with the expected magic token."""
+
+
+class BadHeader(SsimkitError):
+    """Header could not be parsed."""
+
+
+class UnsupportedChroma(SsimkitError):
+    """Chroma subsampling tag is not supported."""
+
+
+class TruncatedFrame(SsimkitError):
+    """Frame payload is shorter than the declared plane sizes."""
+
+
+class SizeNotMultiple(SsimkitError):
+    """Raw file size is not a whole multiple of the frame size."""

@@ -1,0 +1,202 @@
+"""Media ingest straight into the scoring batches (ssimkit src/media.py:94-212).
+
+Y4M (8-bit; YUV4MPEG2 header, FRAME markers) and headerless planar YUV
+(8-bit, or little-endian 16-bit) are memory-mapped; frame offsets are found
+once, and each frame's planes are zero-copy ``numpy`` views into the mapping,
+so batches are filled by one copy per plane into the pinned staging buffers of
+``SequenceScorer`` (no per-frame parsing on the hot loop).  Header grammar,
+chroma tags and error classes follow the reference readers.
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+from typing import Iterator, Optional, Sequence
+
+import numpy as np
+
+from .errors import BadHeader, BadMagic, SizeNotMultiple, TruncatedFrame, UnsupportedChroma, ValidationError
+from .planes import CHROMA_420, CHROMA_444
+
+Y4M_MAGIC = b"YUV4MPEG2"
+_Y4M_CHROMA = {"420": CHROMA_420, "420jpeg": CHROMA_420, "420mpeg2": CHROMA_420, "444": CHROMA_444, "mono": "mono"}
+
+
+@dataclass(frozen=True)
+class StreamHeader:
+    width: int
+    height: int
+    frame_rate: tuple
+    chroma: str  # "420" | "444" | "mono"
+    bit_depth: int = 8
+
+    @property
+    def fps(self) -> float:
+        return self.frame_rate[0] / self.frame_rate[1]
+
+    def plane_shapes(self) -> list:
+        if self.chroma == "mono":
+            return [(self.height, self.width)]
+        if self.chroma == CHROMA_420:
+            c = ((self.height + 1) // 2, (self.width + 1) // 2)
+        else:
+            c = (self.height, self.width)
+        return [(self.height, self.width), c, c]
+
+    @property
+    def sample_dtype(self):
+        return np.dtype(np.uint8) if self.bit_depth <= 8 else np.dtype("<u2")
+
+    def frame_bytes(self) -> int:
+        es = self.sample_dtype.itemsize
+        return sum(h * w * es for h, w in self.plane_shapes())
+
+
+class FrameSource:
+    """Memory-mapped frames of one stream; ``planes(i)`` gives views into the file."""
+
+    def __init__(self, path, header: StreamHeader, offsets: Sequence[int]):
+        self.path = str(path)
+        self.header = header
+        self._offsets = list(offsets)
+        # np.memmap keeps the mapping alive for as long as any returned plane view exists
+        size = os.path.getsize(self.path)
+        self._buf = np.memmap(self.path, dtype=np.uint8, mode="r") if size else np.zeros(0, np.uint8)
+
+    def __len__(self) -> int:
+        return len(self._offsets)
+
+    def planes(self, i: int) -> tuple:
+        off = self._offsets[i]
+        es = self.header.sample_dtype.itemsize
+        out = []
+        for h, w in self.header.plane_shapes():
+            n = h * w * es
+            out.append(self._buf[off:off + n].view(self.header.sample_dtype).reshape(h, w))
+            off += n
+        return tuple(out)
+
+    def luma(self) -> Iterator[np.ndarray]:
+        for i in range(len(self)):
+            yield self.planes(i)[0]
+
+    def frames(self) -> Iterator[tuple]:
+        for i in range(len(self)):
+            yield self.planes(i)
+
+    def close(self) -> None:
+        """Drop this source's reference to the mapping (views handed out stay valid)."""
+        self._buf = np.zeros(0, np.uint8)
+
+
+def _parse_y4m_header(line: str) -> StreamHeader:
+    width = height = None
+    rate = (30, 1)
+    chroma = CHROMA_420
+    for tok in line.split(" "):
+        if not tok:
+            continue
+        tag, val = tok[0], tok[1:]
+        if tag == "W":
+            width = int(val)
+        elif tag == "H":
+            height = int(val)
+        elif tag == "F":
+            num, _, den = val.partition(":")
+            rate = (int(num), int(den or "1"))
+        elif tag == "C":
+            if val not in _Y4M_CHROMA:
+                raise UnsupportedChroma(f"chroma tag C{val} is not supported")
+            chroma = _Y4M_CHROMA[val]
+        elif tag in ("I", "A", "X"):
+            continue
+        else:
+            raise BadHeader(f"unknown header token {tok!r}")
+    if not width or not height or width <= 0 or height <= 0:
+        raise BadHeader(f"header lacks valid dimensions: {line!r}")
+    return StreamHeader(width, height, rate, chroma, 8)
+
+
+def open_y4m(path) -> FrameSource:
+    """Index a YUV4MPEG2 file (src/media.py:94-175): one pass over the FRAME markers."""
+    with open(path, "rb") as fh:
+        data = fh.read()
+    if not data.startswith(Y4M_MAGIC):
+        raise BadMagic(f"{path}: not a YUV4MPEG2 stream")
+    eol = data.find(b"\n")
+    if eol < 0 or eol > 512:
+        raise BadHeader("unterminated header line")
+    header = _parse_y4m_header(data[len(Y4M_MAGIC):eol].decode("ascii", "replace"))
+    fbytes = header.frame_bytes()
+    pos, offsets = eol + 1, []
+    while pos < len(data):
+        nl = data.find(b"\n", pos, pos + 512)
+        if nl < 0:
+            raise BadHeader("unterminated FRAME marker")
+        if not data[pos:nl].startswith(b"FRAME"):
+            raise BadHeader(f"expected FRAME marker, got {data[pos:pos + 20]!r}")
+        start = nl + 1
+        if start + fbytes > len(data):
+            raise TruncatedFrame(f"frame needs {fbytes} bytes, stream had {len(data) - start}")
+        offsets.append(start)
+        pos = start + fbytes
+    return FrameSource(path, header, offsets)
+
+
+def open_raw(path, width: int, height: int, bit_depth: int = 8, chroma: str = CHROMA_420,
+             frame_rate=(30, 1)) -> FrameSource:
+    """Index a headerless planar YUV file (src/media.py:178-212)."""
+    if width <= 0 or height <= 0:
+        raise ValidationError("dimensions must be positive")
+    if chroma == "400":
+        chroma = "mono"
+    if chroma not in (CHROMA_420, CHROMA_444, "mono"):
+        raise UnsupportedChroma(f"chroma {chroma!r} not supported for raw input")
+    header = StreamHeader(width, height, tuple(frame_rate), chroma, bit_depth)
+    fbytes = header.frame_bytes()
+    size = os.path.getsize(path)
+    if size == 0 or size % fbytes != 0:
+        raise SizeNotMultiple(f"{path}: {size} bytes is not a whole number of {fbytes}-byte frames")
+    return FrameSource(path, header, [i * fbytes for i in range(size // fbytes)])
+
+
+def write_y4m(path, frames, width: int, height: int, chroma: str = CHROMA_420, frame_rate=(30, 1)) -> None:
+    """Write 8-bit frames (tuples of planes, or luma planes for mono) as YUV4MPEG2."""
+    tag = {CHROMA_420: "420jpeg", CHROMA_444: "444", "mono": "mono"}[chroma]
+    with open(path, "wb") as fh:
+        fh.write(Y4M_MAGIC + f" W{width} H{height} F{frame_rate[0]}:{frame_rate[1]} C{tag}\n".encode())
+        for fr in frames:
+            fh.write(b"FRAME\n")
+            for p in (fr if isinstance(fr, (tuple, list)) else (fr,)):
+                fh.write(np.ascontiguousarray(p, dtype=np.uint8).tobytes())
+
+
+def write_planar_raw(path, frames, bit_depth: int = 8) -> None:
+    """Write frames as headerless planar YUV (little-endian for > 8 bits)."""
+    dt = np.uint8 if bit_depth <= 8 else np.dtype("<u2")
+    with open(path, "wb") as fh:
+        for fr in frames:
+            for p in (fr if isinstance(fr, (tuple, list)) else (fr,)):
+                fh.write(np.ascontiguousarray(p, dtype=dt).tobytes())
+
+
+def score_files(ref: FrameSource, dist: FrameSource, config=None, batch_frames: int = 16,
+                color_weights: Optional[Sequence[float]] = None):
+    """Score two indexed streams frame by frame on the GPU (the reference's run_score frame loop,
+    src/pipeline.py:275-366, for the luma / multiscale / fixed-weight color models)."""
+    from .options import SsimConfig
+    from .video import SequenceScorer
+
+    config = config or SsimConfig()
+    if (ref.header.width, ref.header.height) != (dist.header.width, dist.header.height):
+        from .errors import DimensionMismatch
+
+        raise DimensionMismatch("reference and distorted streams differ in size")
+    if len(ref) != len(dist):
+        raise ValidationError(f"streams differ in length: {len(ref)} vs {len(dist)} frames")
+    cfg = config.for_bit_depth(ref.header.bit_depth)
+    scorer = SequenceScorer(cfg, batch_frames, color_weights)
+    if color_weights is not None:
+        return scorer.score(ref.frames(), dist.frames())
+    return scorer.score(ref.luma(), dist.luma())

@@ -526,3 +526,21 @@ def test_score_frame_pair_contract(cuda, oracle, rng, golden):
         P.score_frame_pair(a, b, P.SsimConfig(color=P.ColorModelSpec("qssim")))
     with pytest.raises(ValidationError):
         P.score_frame_pair(a, b, P.SsimConfig(scaling=P.ScalePolicy.legacy256()))
+
+
+def test_score_files_y4m(cuda, oracle, tmp_path):
+    from paper_2101_06354_b200 import ingest, synth
+
+    vid = synth.VideoConfig3(frames=5, h=48, w=64)
+    pairs = [vid.pair(t) for t in range(5)]
+    ingest.write_y4m(tmp_path / "r.y4m", [r for r, _ in pairs], 64, 48)
+    ingest.write_y4m(tmp_path / "d.y4m", [d for _, d in pairs], 64, 48)
+    ref, dist = ingest.open_y4m(tmp_path / "r.y4m"), ingest.open_y4m(tmp_path / "d.y4m")
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    wts = (4 / 6, 1 / 6, 1 / 6)
+    res = ingest.score_files(ref, dist, cfg, batch_frames=2, color_weights=wts)
+    win = dict(shape="gauss", k=11, sigma=1.5)
+    want = [oracle.fixed_weight(oracle.channel_scores(r, d, **win), wts) for r, d in pairs]
+    assert np.max(np.abs(res.scores - np.array(want))) < 1e-5
+    luma = ingest.score_files(ref, dist, cfg, batch_frames=3)
+    assert np.max(np.abs(luma.scores - np.array([oracle.ssim_score(r[0], d[0], **win) for r, d in pairs]))) < 1e-5

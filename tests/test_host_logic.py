@@ -167,3 +167,37 @@ def test_no_cpu_fallback():
     with pytest.raises(E.EngineUnavailable):
         P.msssim(np.zeros((64, 64), dtype=np.uint8), np.zeros((64, 64), dtype=np.uint8),
                  P.SsimConfig(window=P.WindowSpec.rectangular(3)), P.MultiscaleSpec.product(3))
+
+
+def test_media_ingest_y4m_and_raw(tmp_path):
+    from paper_2101_06354_b200 import errors as E
+    from paper_2101_06354_b200 import ingest
+
+    rng = np.random.default_rng(5)
+    frames = [(rng.integers(0, 256, (6, 8)).astype(np.uint8), rng.integers(0, 256, (3, 4)).astype(np.uint8),
+               rng.integers(0, 256, (3, 4)).astype(np.uint8)) for _ in range(3)]
+    p = tmp_path / "a.y4m"
+    ingest.write_y4m(p, frames, 8, 6)
+    src = ingest.open_y4m(p)
+    assert len(src) == 3 and src.header.chroma == "420" and src.header.width == 8
+    for i, fr in enumerate(frames):
+        for got, want in zip(src.planes(i), fr):
+            assert np.array_equal(got, want)
+    src.close()
+    r = tmp_path / "a.yuv"
+    ingest.write_planar_raw(r, [tuple(x.astype(np.uint16) * 4 for x in fr) for fr in frames], bit_depth=10)
+    raw = ingest.open_raw(r, 8, 6, bit_depth=10)
+    assert len(raw) == 3 and np.array_equal(raw.planes(2)[1], frames[2][1].astype(np.uint16) * 4)
+    raw.close()
+    with pytest.raises(E.SizeNotMultiple):
+        ingest.open_raw(r, 8, 5, bit_depth=10)
+    bad = tmp_path / "bad.y4m"
+    bad.write_bytes(b"NOTY4M W8 H6\n")
+    with pytest.raises(E.BadMagic):
+        ingest.open_y4m(bad)
+    bad.write_bytes(b"YUV4MPEG2 W8 H6 C411\n")
+    with pytest.raises(E.UnsupportedChroma):
+        ingest.open_y4m(bad)
+    bad.write_bytes(b"YUV4MPEG2 W8 H6\nFRAME\n" + b"\0" * 10)
+    with pytest.raises(E.TruncatedFrame):
+        ingest.open_y4m(bad)
