@@ -18,6 +18,8 @@ scoring, in frame order.
 
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 from typing import Iterable, Optional, Sequence
 
@@ -78,6 +80,11 @@ def gather_frame_scores(local: np.ndarray, n_frames: int, group=None) -> np.ndar
     return np.concatenate(out)
 
 
+def _copy_into(job) -> None:
+    dst, src = job
+    np.copyto(dst, src, casting="unsafe")
+
+
 class SequenceScorer:
     """Score a stream of frame pairs on one GPU.
 
@@ -96,6 +103,7 @@ class SequenceScorer:
         torch = nat.torch_mod()
         self.copy_stream = torch.cuda.Stream(device=self.device)
         self._slots = [None, None]
+        self._copier = ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
         self._events = [None, None]   # upload of the slot finished (host buffer reusable)
         self._done = [None, None]     # scoring of the slot finished (device buffer reusable)
 
@@ -109,29 +117,39 @@ class SequenceScorer:
         for p in range(nplanes):
             r0 = np.asarray(frames[0][0][p] if nplanes == 3 else frames[0][0])
             shapes.append((r0.shape, r0.dtype))
-        key = (len(frames), tuple(s for s, _ in shapes), tuple(str(d) for _, d in shapes))
+        # slot buffers hold batch_frames frames and are reused for shorter (final) batches:
+        # pinned allocations are expensive, so they happen once per geometry
+        key = (tuple(s for s, _ in shapes), tuple(str(d) for _, d in shapes))
         slot_bufs = self._slots[slot]
         if slot_bufs is None or slot_bufs[0] != key:
             bufs = []
             for (h, w), dt in shapes:
                 t_dt = torch.uint8 if dt == np.uint8 else torch.uint16
                 pitch = nat.aligned_pitch(w, nat.U8 if dt == np.uint8 else nat.U16)
-                host = torch.zeros((2, len(frames), h, pitch), dtype=t_dt, pin_memory=True)
+                host = torch.empty((2, self.batch_frames, h, pitch), dtype=t_dt, pin_memory=True)
                 dev = torch.empty_like(host, device=self.device)
                 bufs.append((host, dev, w))
             slot_bufs = (key, bufs)
             self._slots[slot] = slot_bufs
+        nf = len(frames)
+        slot_bufs = (slot_bufs[0], [(host[:, :nf], dev[:, :nf], w) for host, dev, w in slot_bufs[1]])
         if self._events[slot] is not None:
             self._events[slot].synchronize()  # host slot free again (its upload finished)
         nbytes = 0
         with torch.cuda.stream(self.copy_stream):
             if self._done[slot] is not None:
                 self.copy_stream.wait_event(self._done[slot])
+            # pack all planes of the batch into the pinned slot with a thread pool (numpy
+            # copies release the GIL, so the host memcpy runs on several cores), then
+            # issue one async H2D per plane
+            jobs = []
             for p, (host, dev, w) in enumerate(slot_bufs[1]):
                 hv = host.numpy()
                 for i, (r, d) in enumerate(frames):
-                    hv[0, i, :, :w] = r[p] if nplanes == 3 else r
-                    hv[1, i, :, :w] = d[p] if nplanes == 3 else d
+                    jobs.append((hv[0, i, :, :w], r[p] if nplanes == 3 else r))
+                    jobs.append((hv[1, i, :, :w], d[p] if nplanes == 3 else d))
+            list(self._copier.map(_copy_into, jobs))
+            for p, (host, dev, w) in enumerate(slot_bufs[1]):
                 dev.copy_(host, non_blocking=True)
                 nbytes += host.numel() * host.element_size()
                 planes_ref.append(dev[0, :, :, :w])

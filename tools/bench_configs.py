@@ -1,0 +1,101 @@
+"""Throughput of the other BASELINE.json configurations (not the driver's bench line).
+
+  config1: 512x512 u8 Gaussian SSIM, one pair per call (latency of the per-pair API)
+  config3: 1080p YUV420 video, per-plane Gaussian SSIM, fixed weights (4,1,1)/6, temporal mean,
+           through SequenceScorer (numpy frames -> pinned ring -> H2D -> kernels)
+  config4: 4K 10-bit u16 rect 8 stride 4 (integral engine semantics), device-resident batches
+  config5: 4K u8 Gaussian SSIM + 5-scale MS-SSIM per pair, device-resident batches
+
+Seeded pools of distinct pairs are cycled to fill the batches (generation of
+4K 1/f-noise pairs is CPU-heavy); the pool size is printed.  Prints one JSON
+object per configuration.
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+
+def timed(fn, reps: int) -> float:
+    import torch
+
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps / 1e3
+
+
+def main() -> None:
+    import numpy as np
+    import torch
+
+    import bench
+    import paper_2101_06354_b200 as P
+    from paper_2101_06354_b200 import synth
+
+    dev = torch.device("cuda", 0)
+    out = {}
+
+    # config 1: per-pair API latency (host arrays in, score out)
+    a, b = synth.config1_pair()
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    P.ssim_score(a, b, cfg)
+    t0 = time.perf_counter()
+    for _ in range(50):
+        s = P.ssim_score(a, b, cfg)
+    dt = (time.perf_counter() - t0) / 50
+    out["config1"] = {"score": s, "ms_per_call": dt * 1e3, "path": "ssim_score(host numpy, 512x512 u8)"}
+
+    # config 4: 4K 10-bit box windows, HBM-bound
+    pool = [synth.config4_pair(i) for i in range(4)]
+    n = 32
+    ref = torch.from_numpy(np.stack([pool[i % 4][0] for i in range(n)])).to(dev)
+    dist = torch.from_numpy(np.stack([pool[i % 4][1] for i in range(n)])).to(dev)
+    cfg4 = P.SsimConfig(bit_depth=10, window=P.WindowSpec.rectangular(8, stride=4), engine="integral")
+    sec = timed(lambda: P.ssim_terms_batch(ref, dist, cfg4), 20)
+    bytes_per_pair = 2 * 2160 * 3840 * 2
+    out["config4"] = {"pairs_per_s": n / sec, "hbm_GBps": n * bytes_per_pair / sec / 1e9,
+                      "hbm_frac_of_6552": n * bytes_per_pair / sec / 1e9 / 6552.3, "batch": n, "pool": 4}
+    del ref, dist
+
+    # config 5: 4K u8 SSIM + MS-SSIM
+    pool = [synth.dct_pair(5, i, 2160, 3840) for i in range(8)]
+    n = 32
+    ref = torch.from_numpy(np.stack([pool[i % 8][0] for i in range(n)])).to(dev)
+    dist = torch.from_numpy(np.stack([pool[i % 8][1] for i in range(n)])).to(dev)
+    spec = P.MultiscaleSpec.product(5)
+    sec = timed(lambda: P.msssim_batch(ref, dist, cfg, spec, with_ssim=True), 10)
+    flops = n * bench.msssim_flops(2160, 3840)
+    out["config5"] = {"pairs_per_s": n / sec, "TFLOPs": flops / sec / 1e12, "batch": n, "pool": 8,
+                      "note": "4800 pairs would take %.3f s on one GPU" % (4800 / (n / sec))}
+    del ref, dist
+
+    # config 3: YUV420 video through the frame-stream API (host frames -> pinned ring -> GPU)
+    nfr = 300
+    vid = synth.VideoConfig3(frames=nfr)
+    pairs = [vid.pair(t) for t in range(nfr)]
+    scorer = P.SequenceScorer(cfg, batch_frames=16, color_weights=(4 / 6, 1 / 6, 1 / 6))
+    scorer.score([r for r, _ in pairs[:32]], [d for _, d in pairs[:32]])  # warm both pinned slots
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = scorer.score([r for r, _ in pairs], [d for _, d in pairs])
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    out["config3"] = {"frames_per_s_e2e": nfr / dt, "pooled": res.pooled, "frames": nfr,
+                      "h2d_bytes": res.h2d_bytes, "path": "SequenceScorer(color_weights=(4,1,1)/6), host numpy frames"}
+    for k, v in out.items():
+        print(json.dumps({"config": k, **v}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
