@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SSK_ABI_VERSION 4
+#define SSK_ABI_VERSION 5
 
 /* sample storage types */
 enum {
@@ -205,6 +205,61 @@ size_t ssk_volume_workspace_bytes(const ssk_volume* v, const ssk_window* win);
  * as in ssk_ssim; optional float64 maps (SSK_MAP_TERMS / SSK_MAP_STATS). */
 int ssk_volume_ssim(const ssk_volume* v, const ssk_window* win, int want, double* d_sums, void* d_maps,
                     void* d_workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Resolution adaptation: integer-factor block averaging
+ * (box_downsample, src/adaptation.py:93-110).  Output (ceil(h/f), ceil(w/f));
+ * trailing partial blocks average over their actual size.
+ *   dst_dtype SSK_F64: sum / (rows*cols) with one IEEE division -- bit-identical
+ *                      to the reference for integer samples (exact sums);
+ *   dst_dtype SSK_U16 / SSK_U32: the exact block sums of integer samples (the
+ *                      caller must have h % f == 0 and w % f == 0; for a power
+ *                      of two f the result is a scaled plane with
+ *                      scale_log2 = src scale_log2 + 2*log2(f)).
+ */
+int ssk_box_downsample(const ssk_planes* src, int factor, void* d_dst_ref, void* d_dst_dist, int dst_dtype,
+                       int64_t dst_row_pitch, int64_t dst_frame_pitch, void* stream);
+
+/*
+ * Spatial pooling of a batch of quality maps on the device
+ * (pool_spatial, src/pooling.py:157-243).  Kinds follow SPATIAL_KINDS (:29).
+ * Order statistics (fns quartiles, pp cutoff) are exact: a radix select on
+ * the values' order-preserving bit patterns, interpolated with numpy's
+ * 'linear' percentile rule (virtual index n*q + (1 - q) - 1, lerp flipped at
+ * gamma >= 0.5), so they equal np.percentile bit for bit.
+ */
+enum {
+  SSK_POOL_AM = 0,   /* mean                                                */
+  SSK_POOL_COV = 1,  /* std / mean (NaN result for a zero mean: ZeroMeanCoV) */
+  SSK_POOL_MD = 2,   /* (mean |v - mean|^p)^(1/p) ^ o                        */
+  SSK_POOL_FNS = 3,  /* (min + Q1 + median + Q3 + max) / 5                    */
+  SSK_POOL_DW = 4,   /* sum((1-v)^p v) / sum((1-v)^p), mean if all v == 1    */
+  SSK_POOL_MINK = 5, /* mean (1-v)^p                                          */
+  SSK_POOL_LW = 6,   /* mean w(mu) v, w = [mu >= a] (b == 0) or clip((mu-a)/b) */
+  SSK_POOL_PP = 7    /* mean of v/rs below the ps-th percentile, v above     */
+};
+
+typedef struct ssk_maps {
+  const void* values;        /* device quality values                                    */
+  const void* aux;           /* device mean-luminance map (SSK_POOL_LW only), else NULL  */
+  int32_t dtype;             /* SSK_F32 or SSK_F64 (values and aux)                      */
+  int32_t n, h, w;           /* maps, rows, columns                                      */
+  int64_t row_pitch, frame_pitch;          /* elements                                   */
+  int64_t aux_row_pitch, aux_frame_pitch;  /* elements                                   */
+} ssk_maps;
+
+typedef struct ssk_pooler {
+  int32_t kind;              /* SSK_POOL_*                                               */
+  int32_t _pad;
+  double p, o;               /* md / dw / mink exponent, md outer exponent               */
+  double a, b;               /* lw lower luminance limit, ramp length                    */
+  double ps, rs;             /* pp percentile, down-weighting divisor                    */
+} ssk_pooler;
+
+size_t ssk_pool_workspace_bytes(const ssk_maps* m, const ssk_pooler* pool);
+/* d_out [n] pooled scores; d_mean [n] (nullable) the plain mean of each map. */
+int ssk_pool_spatial(const ssk_maps* m, const ssk_pooler* pool, double* d_out, double* d_mean,
+                     void* d_workspace, size_t workspace_bytes, void* stream);
 
 /* Number of kernels this library has launched since load (for bench.py). */
 uint64_t ssk_launch_count(void);

@@ -16,6 +16,10 @@ order, so that its outputs are bit-identical to the reference's:
   scale_scores / combine . src/multiscale.py:36-74
   channel_scores ......... src/color.py:111-153         (cw / fixed models)
   pool_temporal_am ....... src/pooling.py:254-255
+  scale factors .......... src/adaptation.py:23-90      (256-line rule, dh, sast)
+  box_downsample ......... src/adaptation.py:93-110     (block means, ragged edges)
+  pool_spatial ........... src/pooling.py:157-243       (am cov md fns dw mink lw pp)
+  luma_frame_record ...... src/pipeline.py:197-236      (scale -> stats -> pool record)
 
 Parity pinning: tests/test_oracle_golden.py checks this module against
 golden vectors produced by the reference itself (tests/golden/make_golden.py,
@@ -307,3 +311,92 @@ def msssim3d(ref_frames, dist_frames, kt: int, levels: int = 5, aggregation: str
             per.append(float((q if lv == levels - 1 else cs_map).mean()))
         out.append(combine_scale_scores(per, aggregation, exponents))
     return out
+
+
+# ---------------------------------------------------------------------------
+# resolution adaptation (src/adaptation.py:23-110)
+# ---------------------------------------------------------------------------
+
+def round_half_away(x: float) -> int:
+    return int(math.floor(x + 0.5)) if x >= 0 else -int(math.floor(-x + 0.5))
+
+
+def scale_factor(kind: str, width: int, height: int, rounding: str = "round", d_over_h: float = 3.0,
+                 distance: float | None = None, theta_h: float = 40.0, theta_w: float = 50.0) -> int:
+    """Integer factor of a scale policy: none / legacy (256-line rule) / dh / sast."""
+    if kind == "none":
+        return 1
+    if kind in ("legacy", "dh"):
+        ratio = min(width, height) / 256.0
+        if kind == "dh":
+            ratio = ratio * (3.0 / d_over_h)
+        r = math.ceil(ratio) if rounding == "ceil" else round_half_away(ratio)
+        return max(1, r)
+    denom = 4.0 * math.tan(math.radians(theta_h) / 2.0) * math.tan(math.radians(theta_w) / 2.0)
+    z = max(1.0, math.sqrt((height / distance) * (width / distance) / denom))
+    return max(1, round_half_away(z))
+
+
+def box_downsample(values: np.ndarray, factor: int) -> np.ndarray:
+    """Block means over factor x factor blocks; trailing blocks average their real size."""
+    if factor == 1:
+        return values
+    x = np.asarray(values, dtype=np.float64)
+    h, w = x.shape
+    rows, cols = np.arange(0, h, factor), np.arange(0, w, factor)
+    block = np.add.reduceat(np.add.reduceat(x, rows, axis=0), cols, axis=1)
+    counts = np.outer(np.minimum(rows + factor, h) - rows, np.minimum(cols + factor, w) - cols)
+    return block / counts
+
+
+# ---------------------------------------------------------------------------
+# spatial pooling (src/pooling.py:157-243)
+# ---------------------------------------------------------------------------
+
+def pool_spatial(values, kind: str, p: float = 1.0, o: float = 1.0, a: float = 0.0, b: float = 0.0,
+                 ps: float = 6.0, rs: float = 1.0, ref_luma=None) -> float:
+    v = np.asarray(values, dtype=np.float64).reshape(-1)
+    if v.size == 0:
+        raise ValueError("empty map")
+    if kind == "am":
+        return float(v.mean())
+    if kind == "cov":
+        m = v.mean()
+        if m == 0.0:
+            raise ZeroDivisionError("zero-mean map")
+        return float(v.std() / m)
+    if kind == "md":
+        spread = (np.abs(v - v.mean()) ** p).mean()
+        return float((spread ** (1.0 / p)) ** o)
+    if kind == "fns":
+        lo, mid, hi = np.percentile(v, [25.0, 50.0, 75.0])
+        return float((v.min() + lo + mid + hi + v.max()) / 5.0)
+    if kind == "dw":
+        wt = (1.0 - v) ** p
+        tot = wt.sum()
+        return float(v.mean()) if tot == 0.0 else float((wt * v).sum() / tot)
+    if kind == "mink":
+        return float(((1.0 - v) ** p).mean())
+    if kind == "pp":
+        if ps <= 0.0 or rs == 1.0:
+            return float(v.mean())
+        cut = np.percentile(v, ps)
+        return float(np.where(v <= cut, v / rs, v).mean())
+    if kind == "lw":
+        mu = np.asarray(ref_luma, dtype=np.float64).reshape(-1)
+        wt = (mu >= a).astype(np.float64) if b == 0.0 else np.clip((mu - a) / b, 0.0, 1.0)
+        return float((wt * v).mean())
+    raise ValueError(f"unknown pooler {kind!r}")
+
+
+def luma_frame_record(ref, dist, shape: str = "rect", k: int = 11, stride: int = 1, sigma: float | None = None,
+                      bit_depth: int = 8, engine: str = "auto", factor: int = 1, pool: str = "am",
+                      **pool_params) -> tuple[float, float, float, float]:
+    """(score, am, l_mean, cs_mean) of one luma pair: downsample, statistics, maps, pooling."""
+    x = box_downsample(np.asarray(ref), factor)
+    y = box_downsample(np.asarray(dist), factor)
+    stats = local_statistics(x, y, shape, k, stride, sigma, engine)
+    c1, c2 = constants(bit_depth)
+    l_map, cs_map, q = term_maps(*stats, c1, c2)
+    score = pool_spatial(q, pool, ref_luma=stats[0], **pool_params)
+    return score, float(q.mean()), float(l_map.mean()), float(cs_map.mean())

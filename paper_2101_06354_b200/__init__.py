@@ -47,7 +47,17 @@ from .options import (
     parse_window,
 )
 from .planes import ColorFrame, LumaPlane, QualityMap, ScoreSeries, validate_frame_pair
-from .pooling import SpatialPooler, TemporalPooler, pool_spatial, pool_temporal
+from .pooling import SpatialPooler, TemporalPooler, parse_spatial, parse_temporal, pool_maps, pool_spatial, pool_temporal
+from .adaptation import (
+    box_downsample,
+    enhanced_scale_factor,
+    legacy_scale_factor,
+    policy_factor,
+    round_half_away,
+    sast_factor,
+    viewing_geometry,
+)
+from .pipeline import FrameRecords, PipelineSpec, expand_preset, luma_records, preset_specs, score_batch
 from .pyramid import combine_scale_scores, dyadic_downsample, msssim, scale_scores
 from .scoring import (
     SsimTermMaps,
@@ -83,7 +93,13 @@ __all__ = [
     "channel_scores", "channelwise_cssim", "combine_channelwise", "fixed_weight_cssim", "luma_of",
     "rgb_to_ycbcr_bt709", "upsample_chroma", "ycbcr_bt709_to_rgb",
     # pooling
-    "SpatialPooler", "TemporalPooler", "pool_spatial", "pool_temporal",
+    "SpatialPooler", "TemporalPooler", "parse_spatial", "parse_temporal", "pool_maps", "pool_spatial",
+    "pool_temporal",
+    # resolution adaptation
+    "box_downsample", "enhanced_scale_factor", "legacy_scale_factor", "policy_factor", "round_half_away",
+    "sast_factor", "viewing_geometry",
+    # pipeline contract / presets
+    "FrameRecords", "PipelineSpec", "expand_preset", "luma_records", "preset_specs", "score_batch",
     # batched device API / sequences / multi-GPU
     "FrameTerms", "HostBatchScorer", "color_batch", "msssim_batch", "ssim_batch", "ssim_terms_batch",
     "SequenceScorer", "gather_frame_scores", "score_sequence", "shard_bounds", "FrameScore", "score_frame_pair",

@@ -32,7 +32,7 @@ RECT, GAUSS = 1, 2
 WANT_Q, WANT_L, WANT_CS, MAP_TERMS, MAP_STATS = 1, 2, 4, 8, 16
 E_ARG, E_WINDOW, E_SHAPE, E_WORKSPACE, E_ALIGN, E_CUDA, E_LEVELS, E_TOO_SMALL = range(-1, -9, -1)
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 EXPORTED_SYMBOLS = (
     "ssk_abi_version",
@@ -48,9 +48,15 @@ EXPORTED_SYMBOLS = (
     "ssk_volume_refresh",
     "ssk_volume_workspace_bytes",
     "ssk_volume_ssim",
+    "ssk_box_downsample",
+    "ssk_pool_workspace_bytes",
+    "ssk_pool_spatial",
     "ssk_launch_count",
     "ssk_probe_fp32_tflops",
 )
+
+# spatial pooler kinds (SSK_POOL_*), in SPATIAL_KINDS order of src/pooling.py:29
+POOL_KINDS = {"am": 0, "cov": 1, "md": 2, "fns": 3, "dw": 4, "mink": 5, "lw": 6, "pp": 7}
 
 
 class Planes(ctypes.Structure):
@@ -76,6 +82,34 @@ class Volume(ctypes.Structure):
         ("w", ctypes.c_int32),
         ("depth", ctypes.c_int32),
         ("pitch", ctypes.c_int64),
+    ]
+
+
+class Maps(ctypes.Structure):
+    _fields_ = [
+        ("values", ctypes.c_void_p),
+        ("aux", ctypes.c_void_p),
+        ("dtype", ctypes.c_int32),
+        ("n", ctypes.c_int32),
+        ("h", ctypes.c_int32),
+        ("w", ctypes.c_int32),
+        ("row_pitch", ctypes.c_int64),
+        ("frame_pitch", ctypes.c_int64),
+        ("aux_row_pitch", ctypes.c_int64),
+        ("aux_frame_pitch", ctypes.c_int64),
+    ]
+
+
+class Pooler(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
+        ("p", ctypes.c_double),
+        ("o", ctypes.c_double),
+        ("a", ctypes.c_double),
+        ("b", ctypes.c_double),
+        ("ps", ctypes.c_double),
+        ("rs", ctypes.c_double),
     ]
 
 
@@ -134,6 +168,13 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         lib.ssk_volume_workspace_bytes.argtypes = [pV, pW]
         lib.ssk_volume_ssim.restype = i32
         lib.ssk_volume_ssim.argtypes = [pV, pW, i32, vp, vp, vp, sz, vp]
+        lib.ssk_box_downsample.restype = i32
+        lib.ssk_box_downsample.argtypes = [pP, i32, vp, vp, i32, i64, i64, vp]
+        pM, pQ = ctypes.POINTER(Maps), ctypes.POINTER(Pooler)
+        lib.ssk_pool_workspace_bytes.restype = sz
+        lib.ssk_pool_workspace_bytes.argtypes = [pM, pQ]
+        lib.ssk_pool_spatial.restype = i32
+        lib.ssk_pool_spatial.argtypes = [pM, pQ, vp, vp, vp, sz, vp]
         lib.ssk_launch_count.restype = ctypes.c_uint64
         lib.ssk_probe_fp32_tflops.restype = i32
         lib.ssk_probe_fp32_tflops.argtypes = [ctypes.c_double, ctypes.POINTER(ctypes.c_double), vp]

@@ -28,8 +28,9 @@ import numpy as np
 from . import _native as nat
 from . import batch as B
 from .errors import EmptySeries, ValidationError
-from .options import MultiscaleSpec, SsimConfig
+from .options import SsimConfig
 from .planes import ScoreSeries
+from .pipeline import FrameScore, luma_records, score_frame_pair  # noqa: F401  (re-exported)
 from .pooling import pool_temporal
 
 
@@ -163,10 +164,11 @@ class SequenceScorer:
         cfg = self.config
         if self.color_weights is not None:
             return B.color_batch(planes_ref, planes_dist, cfg, weights=self.color_weights), None
-        if cfg.multiscale.enabled:
-            return B.msssim_batch(planes_ref[0], planes_dist[0], cfg, cfg.multiscale), None
-        terms = B.ssim_terms_batch(planes_ref[0], planes_dist[0], cfg)
-        return terms.score, terms
+        from . import engine
+
+        pair = engine.device_pair(planes_ref[0], planes_dist[0], cfg.bit_depth, cfg.window.shape == "gauss")
+        rec = luma_records(pair, cfg, strict=False)
+        return rec.score, rec
 
     def score(self, ref_frames: Iterable, dist_frames: Iterable) -> SequenceResult:
         torch = nat.torch_mod()
@@ -196,16 +198,18 @@ class SequenceScorer:
         if batch:
             flush(batch)
         idx = 0
-        for count, score, terms in pending:
+        for count, score, rec in pending:
             s = score.cpu().numpy()
-            if terms is not None:
-                lm, cm = terms.l_mean.cpu().numpy(), terms.cs_mean.cpu().numpy()
+            extra = [None if t is None else t.cpu().numpy() for t in
+                     ((rec.am, rec.l_mean, rec.cs_mean) if rec is not None else (None, None, None))]
             for i in range(count):
-                if terms is not None:
-                    result.records.append(FrameRecord(idx, float(s[i]), float(s[i]), float(lm[i]), float(cm[i])))
-                else:
-                    result.records.append(FrameRecord(idx, float(s[i]), None, None, None))
+                am, lm, cm = (None if e is None else float(e[i]) for e in extra)
+                result.records.append(FrameRecord(idx, float(s[i]), am, lm, cm))
                 idx += 1
+        if self.config.spatial_pool.startswith("cov") and np.isnan(result.scores).any():
+            from .errors import ZeroMeanCoV
+
+            raise ZeroMeanCoV("coefficient of variation is undefined for a zero-mean quality map")
         if not result.records:
             raise EmptySeries("no frames to score")
         result.pooled = pool_temporal(ScoreSeries(result.scores), self.config.temporal_pool)
@@ -216,80 +220,3 @@ def score_sequence(ref_frames, dist_frames, config: SsimConfig = SsimConfig(), b
                    color_weights=None) -> SequenceResult:
     """Convenience wrapper around ``SequenceScorer``."""
     return SequenceScorer(config, batch_frames, color_weights).score(ref_frames, dist_frames)
-
-
-# ---------------------------------------------------------------------------
-# Per-frame contract of the reference pipeline (score_frame_pair, src/pipeline.py:197-258)
-# ---------------------------------------------------------------------------
-
-@dataclass
-class FrameScore:
-    score: float
-    am: Optional[float]
-    l_mean: Optional[float]
-    cs_mean: Optional[float]
-
-
-def score_frame_pair(ref, dist, config: SsimConfig, volume=None) -> FrameScore:
-    """Score one frame pair under a config (src/pipeline.py:197-258) on the device.
-
-    Luma planes: single-scale SSIM with the configured spatial pooler (mean
-    pooling stays fused in the kernel; other poolers pool the device-computed map
-    on the host, with the reference-mean map for luminance weighting), MS-SSIM
-    when ``config.multiscale`` is enabled, or SSIM-3D when a ``RollingVolume`` is
-    given.  YCbCr/RGB ``ColorFrame`` pairs: the channel-wise ``cw`` / ``fixed``
-    models.  Resolution adaptation and the qssim/cmssim/hssim models are not
-    part of the accelerated path and raise ``ValidationError``.
-    """
-    from . import chroma
-    from .errors import DimensionMismatch
-    from .moments import local_statistics
-    from .planes import ColorFrame, LumaPlane, validate_color_pair, validate_frame_pair
-    from .pooling import parse_spatial, pool_spatial
-    from .pyramid import msssim
-    from .scoring import ssim_map, ssim_terms
-
-    if config.scaling.kind != "none":
-        raise ValidationError("resolution adaptation (ScalePolicy) is not part of the accelerated path")
-    luma_ref = not isinstance(ref, ColorFrame)
-    luma_dist = not isinstance(dist, ColorFrame)
-    if luma_ref != luma_dist:
-        raise DimensionMismatch("one stream is luma-only, the other tri-channel")
-    model = config.color.model
-    if luma_ref:
-        validate_frame_pair(ref, dist)
-        if model != "luma":
-            raise ValidationError(f"color model {model!r} needs tri-channel input, stream is luma-only")
-        bd = ref.bit_depth if isinstance(ref, LumaPlane) else config.bit_depth
-        cfg = config.for_bit_depth(bd)
-        if volume is not None:
-            if cfg.multiscale.enabled:
-                raise ValidationError("use run_score for multiscale 3-D pipelines")
-            volume.push(ref, dist)
-            pool = parse_spatial(cfg.spatial_pool)
-            if pool.kind == "am":
-                q, lm, cm = volume.terms(cfg.window, cfg)
-                return FrameScore(q, q, lm, cm)
-            from .volume import ssim3d_map
-
-            maps = ssim3d_map(volume, cfg.window, cfg)
-            mu1 = volume.local_statistics(cfg.window).mu1
-            return FrameScore(pool_spatial(maps.q_map, pool, ref_luma=mu1), float(maps.q_map.values.mean()),
-                              float(maps.l_map.values.mean()), float(maps.cs_map.values.mean()))
-        if cfg.multiscale.enabled:
-            return FrameScore(msssim(ref, dist, cfg, cfg.multiscale), None, None, None)
-        pool = parse_spatial(cfg.spatial_pool)
-        if pool.kind == "am":
-            q, lm, cm = ssim_terms(ref, dist, cfg)
-            return FrameScore(q, q, lm, cm)
-        maps = ssim_map(ref, dist, cfg)
-        mu1 = local_statistics(ref, dist, cfg.window, cfg.engine).mu1
-        return FrameScore(pool_spatial(maps.q_map, pool, ref_luma=mu1), float(maps.q_map.values.mean()),
-                          float(maps.l_map.values.mean()), float(maps.cs_map.values.mean()))
-    validate_color_pair(ref, dist)
-    cfg = config.for_bit_depth(ref.bit_depth)
-    if model == "cw":
-        return FrameScore(chroma.channelwise_cssim(ref, dist, cfg.color.alpha, cfg.color.beta, cfg), None, None, None)
-    if model == "fixed":
-        return FrameScore(chroma.fixed_weight_cssim(ref, dist, cfg.color.weights, cfg), None, None, None)
-    raise ValidationError(f"color model {model!r} is not part of the accelerated path")

@@ -524,8 +524,11 @@ def test_score_frame_pair_contract(cuda, oracle, rng, golden):
     assert abs(r3.score - oracle.ssim_score(a, b, shape="rect", k=7)) < 1e-12
     with pytest.raises(ValidationError):
         P.score_frame_pair(a, b, P.SsimConfig(color=P.ColorModelSpec("qssim")))
-    with pytest.raises(ValidationError):
-        P.score_frame_pair(a, b, P.SsimConfig(scaling=P.ScalePolicy.legacy256()))
+    # resolution adaptation is on the device path now (tests/test_gpu_pool.py); frames
+    # under 384 lines keep factor 1 under the 256-line rule
+    if min(a.shape) < 384:
+        scaled = P.score_frame_pair(a, b, P.SsimConfig(scaling=P.ScalePolicy.legacy256()))
+        assert scaled.score == P.score_frame_pair(a, b, P.SsimConfig()).score
 
 
 def test_score_files_y4m(cuda, oracle, tmp_path):

@@ -108,7 +108,8 @@ class TestContainers:
 
 
 class TestPooling:
-    def test_spatial_known_answers(self):
+    @pytest.mark.gpu
+    def test_spatial_known_answers(self, cuda):
         # tests/test_pooling.py style known answers
         v = np.array([[0.25, 0.5], [0.75, 1.0]])
         assert P.pool_spatial(v, "am") == 0.625
