@@ -188,14 +188,22 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
     a.ch = vr * s;
     a.in_pitch = BX_THREADS * es + 16;
     a.nslot = (k + s - 1) / s + 1;
-    // geometry-only segmentation (~256 input rows), independent of the batch size
-    int seg_anchors = (256 + s - 1) / s;
+    // geometry-only segmentation (~256 input rows; shorter segments, down to ~48 rows,
+    // when a frame would otherwise give fewer than 32 CTAs), independent of the batch size
+    int seg_rows = 256;
+    while (seg_rows > 48 && (long long)nstrips * ((pl.gh + (seg_rows + s - 1) / s - 1) / ((seg_rows + s - 1) / s)) < 32)
+      seg_rows /= 2;
+    int seg_anchors = (seg_rows + s - 1) / s;
     if (seg_anchors < 1) seg_anchors = 1;
     long long nseg = (pl.gh + seg_anchors - 1) / seg_anchors;
     seg_anchors = (int)((pl.gh + nseg - 1) / nseg);
     a.seg_anchors = seg_anchors;
     nseg = (pl.gh + seg_anchors - 1) / seg_anchors;
     if (nseg > 65535) return SSK_E_ARG;
+    // short segments: stage at most ~half a segment per chunk (less shared memory per
+    // CTA -> more resident CTAs to hide the staging latency)
+    const int vr_seg = (seg_anchors + 1) / 2;
+    if (vr > vr_seg) a.ch = (vr_seg < 1 ? 1 : vr_seg) * s;
     pl.grid = dim3(nstrips, (unsigned)nseg, p->n);
     pl.nparts_per_frame = (size_t)nstrips * nseg;
     if (a.na < 1 || box_smem_bytes(a, pl.wide) > 227 * 1024) {

@@ -87,14 +87,14 @@ __device__ __forceinline__ double np_lerp(double lo, double hi, double t) {
 }
 
 // Visit the elements of row range `blk` of one map: f(row, col), block-strided.
-template <typename F>
+template <int NT = PL_THREADS, typename F>
 __device__ __forceinline__ void for_range(const PoolArgs& a, int blk, F&& f) {
   const int r0 = (int)((long long)blk * a.h / a.nblk);
   const int r1 = (int)((long long)(blk + 1) * a.h / a.nblk);
   const long long total = (long long)(r1 - r0) * a.w;
-  const int dr = PL_THREADS / a.w, dc = PL_THREADS % a.w;
+  const int dr = NT / a.w, dc = NT % a.w;
   int row = r0 + (int)(threadIdx.x / a.w), col = (int)(threadIdx.x % a.w);
-  for (long long i = threadIdx.x; i < total; i += PL_THREADS) {
+  for (long long i = threadIdx.x; i < total; i += NT) {
     f(row, col);
     row += dr;
     col += dc;
@@ -136,6 +136,77 @@ __device__ double rank_value(const PoolArgs& a, int frame, int r) {
   return Keys<T>::value(a.sel[((long long)frame * MAX_RANKS + r) * 2]);
 }
 
+// per-element work of the two passes
+template <typename T>
+__device__ __forceinline__ void pass1_elem(const PoolArgs& a, int frame, int row, int col, double& sum, double& mn,
+                                           double& mx, double& f1, double& f2) {
+  const double v = map_at<T>(a.vals, a.fp, a.rp, frame, row, col);
+  sum += v;
+  mn = fmin(mn, v);
+  mx = fmax(mx, v);
+  if (a.kind == SSK_POOL_DW) {
+    const double wt = powp(__dsub_rn(1.0, v), a.p);
+    f1 += wt;
+    f2 += __dmul_rn(wt, v);
+  } else if (a.kind == SSK_POOL_MINK) {
+    f1 += powp(__dsub_rn(1.0, v), a.p);
+  } else if (a.kind == SSK_POOL_LW) {
+    const double mu = map_at<T>(a.aux, a.afp, a.arp, frame, row, col);
+    const double wt = a.b == 0.0 ? (mu >= a.a ? 1.0 : 0.0) : fmin(fmax(__ddiv_rn(__dsub_rn(mu, a.a), a.b), 0.0), 1.0);
+    f1 += __dmul_rn(wt, v);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ double pass2_elem(const PoolArgs& a, int frame, int row, int col, double c) {
+  const double v = map_at<T>(a.vals, a.fp, a.rp, frame, row, col);
+  if (a.kind == SSK_POOL_COV) {
+    const double d = __dsub_rn(v, c);
+    return __dmul_rn(d, d);
+  }
+  if (a.kind == SSK_POOL_MD) return powp(fabs(__dsub_rn(v, c)), a.p);
+  return v <= c ? __ddiv_rn(v, a.rs) : v;  // pp
+}
+
+// pooled score from the folded sums (src/pooling.py:157-243 semantics)
+template <typename T>
+__device__ void finish(const PoolArgs& a, int frame, double sum, double mn, double mx, double f1, double f2,
+                       double s2) {
+  const double mean = __ddiv_rn(sum, a.cnt);
+  double r = mean;
+  switch (a.kind) {
+    case SSK_POOL_COV:
+      r = mean == 0.0 ? NAN : __ddiv_rn(__dsqrt_rn(__ddiv_rn(s2, a.cnt)), mean);
+      break;
+    case SSK_POOL_MD: {
+      const double inner = powp(__ddiv_rn(s2, a.cnt), __ddiv_rn(1.0, a.p));
+      r = a.o == 1.0 ? inner : pow(inner, a.o);
+      break;
+    }
+    case SSK_POOL_FNS: {
+      double q[3];
+      for (int i = 0; i < 3; ++i)
+        q[i] = np_lerp(rank_value<T>(a, frame, 2 * i), rank_value<T>(a, frame, 2 * i + 1), a.gamma[i]);
+      r = __ddiv_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(mn, q[0]), q[1]), q[2]), mx), 5.0);
+      break;
+    }
+    case SSK_POOL_DW:
+      r = f1 == 0.0 ? mean : __ddiv_rn(f2, f1);
+      break;
+    case SSK_POOL_MINK:
+    case SSK_POOL_LW:
+      r = __ddiv_rn(f1, a.cnt);
+      break;
+    case SSK_POOL_PP:
+      r = (a.ps <= 0.0 || a.rs == 1.0) ? mean : __ddiv_rn(s2, a.cnt);
+      break;
+    default:
+      break;
+  }
+  a.out[frame] = r;
+  if (a.mean) a.mean[frame] = mean;
+}
+
 // ---------------------------------------------------------------------------
 // pass 1: sum, min, max and the kind's own sums
 // ---------------------------------------------------------------------------
@@ -149,25 +220,7 @@ __global__ void __launch_bounds__(PL_THREADS) pool_pass1_kernel(const __grid_con
     s[1] = (unsigned long long)a.rank[threadIdx.x];
   }
   double sum = 0.0, mn = INFINITY, mx = -INFINITY, f1 = 0.0, f2 = 0.0;
-  const int kind = a.kind;
-  for_range(a, blk, [&](int row, int col) {
-    const double v = map_at<T>(a.vals, a.fp, a.rp, frame, row, col);
-    sum += v;
-    mn = fmin(mn, v);
-    mx = fmax(mx, v);
-    if (kind == SSK_POOL_DW) {
-      const double wt = powp(__dsub_rn(1.0, v), a.p);
-      f1 += wt;
-      f2 += __dmul_rn(wt, v);
-    } else if (kind == SSK_POOL_MINK) {
-      f1 += powp(__dsub_rn(1.0, v), a.p);
-    } else if (kind == SSK_POOL_LW) {
-      const double mu = map_at<T>(a.aux, a.afp, a.arp, frame, row, col);
-      const double wt = a.b == 0.0 ? (mu >= a.a ? 1.0 : 0.0)
-                                   : fmin(fmax(__ddiv_rn(__dsub_rn(mu, a.a), a.b), 0.0), 1.0);
-      f1 += __dmul_rn(wt, v);
-    }
-  });
+  for_range(a, blk, [&](int row, int col) { pass1_elem<T>(a, frame, row, col, sum, mn, mx, f1, f2); });
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   sum = warp_sum(sum);
   mn = warp_min(mn);
@@ -208,19 +261,8 @@ __global__ void __launch_bounds__(PL_THREADS) pool_pass2_kernel(const __grid_con
   }
   __syncthreads();
   const double c = centre_s;
-  const int kind = a.kind;
   double acc = 0.0;
-  for_range(a, blk, [&](int row, int col) {
-    const double v = map_at<T>(a.vals, a.fp, a.rp, frame, row, col);
-    if (kind == SSK_POOL_COV) {
-      const double d = __dsub_rn(v, c);
-      acc += __dmul_rn(d, d);
-    } else if (kind == SSK_POOL_MD) {
-      acc += powp(fabs(__dsub_rn(v, c)), a.p);
-    } else {  // pp
-      acc += v <= c ? __ddiv_rn(v, a.rs) : v;
-    }
-  });
+  for_range(a, blk, [&](int row, int col) { acc += pass2_elem<T>(a, frame, row, col, c); });
   acc = warp_sum(acc);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
@@ -330,40 +372,59 @@ __global__ void pool_finalize_kernel(const __grid_constant__ PoolArgs a) {
   const double f1 = fold_sum(p1, a.nblk, NC1, 3);
   const double f2 = fold_sum(p1, a.nblk, NC1, 4);
   const double s2 = a.pass2 ? fold_sum(a.part2 + (long long)frame * a.nblk, a.nblk, 1, 0) : 0.0;
-  if (lane) return;
-  const double mean = __ddiv_rn(sum, a.cnt);
-  double r = mean;
-  switch (a.kind) {
-    case SSK_POOL_COV:
-      r = mean == 0.0 ? NAN : __ddiv_rn(__dsqrt_rn(__ddiv_rn(s2, a.cnt)), mean);
-      break;
-    case SSK_POOL_MD: {
-      const double inner = powp(__ddiv_rn(s2, a.cnt), __ddiv_rn(1.0, a.p));
-      r = a.o == 1.0 ? inner : pow(inner, a.o);
-      break;
-    }
-    case SSK_POOL_FNS: {
-      double q[3];
-      for (int i = 0; i < 3; ++i)
-        q[i] = np_lerp(rank_value<T>(a, frame, 2 * i), rank_value<T>(a, frame, 2 * i + 1), a.gamma[i]);
-      r = __ddiv_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(mn, q[0]), q[1]), q[2]), mx), 5.0);
-      break;
-    }
-    case SSK_POOL_DW:
-      r = f1 == 0.0 ? mean : __ddiv_rn(f2, f1);
-      break;
-    case SSK_POOL_MINK:
-    case SSK_POOL_LW:
-      r = __ddiv_rn(f1, a.cnt);
-      break;
-    case SSK_POOL_PP:
-      r = (a.ps <= 0.0 || a.rs == 1.0) ? mean : __ddiv_rn(s2, a.cnt);
-      break;
-    default:
-      break;
+  if (lane == 0) finish<T>(a, frame, sum, mn, mx, f1, f2, s2);
+}
+
+// ---------------------------------------------------------------------------
+// small maps (one block per map, no order statistics): both passes and the
+// final combination in one launch
+// ---------------------------------------------------------------------------
+constexpr int PS_THREADS = 512;
+
+template <typename T>
+__global__ void __launch_bounds__(PS_THREADS) pool_small_kernel(const __grid_constant__ PoolArgs a) {
+  __shared__ double red[PS_THREADS / 32][NC1];
+  __shared__ double tot[NC1];
+  const int frame = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double sum = 0.0, mn = INFINITY, mx = -INFINITY, f1 = 0.0, f2 = 0.0;
+  for_range<PS_THREADS>(a, 0, [&](int row, int col) { pass1_elem<T>(a, frame, row, col, sum, mn, mx, f1, f2); });
+  sum = warp_sum(sum);
+  mn = warp_min(mn);
+  mx = warp_max(mx);
+  f1 = warp_sum(f1);
+  f2 = warp_sum(f2);
+  if (lane == 0) {
+    red[warp][0] = sum;
+    red[warp][1] = mn;
+    red[warp][2] = mx;
+    red[warp][3] = f1;
+    red[warp][4] = f2;
   }
-  a.out[frame] = r;
-  if (a.mean) a.mean[frame] = mean;
+  __syncthreads();
+  if (threadIdx.x < NC1) {
+    const int c = threadIdx.x;
+    double r = red[0][c];
+    for (int wi = 1; wi < PS_THREADS / 32; ++wi)
+      r = c == 1 ? fmin(r, red[wi][c]) : (c == 2 ? fmax(r, red[wi][c]) : r + red[wi][c]);
+    tot[c] = r;
+  }
+  __syncthreads();
+  double s2 = 0.0;
+  if (a.pass2) {
+    const double c = __ddiv_rn(tot[0], a.cnt);
+    double acc = 0.0;
+    for_range<PS_THREADS>(a, 0, [&](int row, int col) { acc += pass2_elem<T>(a, frame, row, col, c); });
+    acc = warp_sum(acc);
+    __syncthreads();
+    if (lane == 0) red[warp][0] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s2 = red[0][0];
+      for (int wi = 1; wi < PS_THREADS / 32; ++wi) s2 += red[wi][0];
+    }
+  }
+  if (threadIdx.x == 0) finish<T>(a, frame, tot[0], tot[1], tot[2], tot[3], tot[4], s2);
 }
 
 // ---------------------------------------------------------------------------
@@ -434,6 +495,78 @@ __global__ void __launch_bounds__(128) box_downsample_kernel(const unsigned char
   if constexpr (std::is_floating_point<TD>::value) *d = (TD)__ddiv_rn(value, (double)((r1 - r0) * (c1 - c0)));
 }
 
+// Vector path (the resolution-adaptation hot case): integer samples, a power-of-two
+// factor F that divides a 16-byte vector, frames tiled by F, 16-byte aligned rows.
+// A thread owns one vector column of F input rows: F independent 16-byte loads,
+// V/F block sums out.
+template <typename TS, typename TD, int F>
+__global__ void __launch_bounds__(128) box_down_vec_kernel(const unsigned char* __restrict__ src_r,
+                                                           const unsigned char* __restrict__ src_d, long long srp,
+                                                           long long sfp, int w, unsigned char* __restrict__ dst_r,
+                                                           unsigned char* __restrict__ dst_d, long long drp,
+                                                           long long dfp, int nvec) {
+  constexpr int V = 16 / (int)sizeof(TS);
+  constexpr int NO = V / F;
+  const int vx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (vx >= nvec) return;
+  const int y = blockIdx.y;
+  const int frame = blockIdx.z >> 1, img = blockIdx.z & 1;
+  const TS* s = reinterpret_cast<const TS*>(img ? src_d : src_r) + (long long)frame * sfp +
+                (long long)(y * F) * srp + (long long)vx * V;
+  uint32_t acc[NO];
+#pragma unroll
+  for (int j = 0; j < NO; ++j) acc[j] = 0u;
+  const int nvalid = min(V, w - vx * V);  // a multiple of F (w % F == 0)
+  if (nvalid == V) {
+    uint4 q[F];
+#pragma unroll
+    for (int r = 0; r < F; ++r) q[r] = __ldg(reinterpret_cast<const uint4*>(s + (long long)r * srp));
+#pragma unroll
+    for (int r = 0; r < F; ++r) {
+      const TS* e = reinterpret_cast<const TS*>(&q[r]);
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[i / F] += (uint32_t)e[i];
+    }
+  } else {
+    for (int r = 0; r < F; ++r)
+      for (int i = 0; i < nvalid; ++i) acc[i / F] += (uint32_t)s[(long long)r * srp + i];
+  }
+  TD* d = reinterpret_cast<TD*>(img ? dst_d : dst_r) + (long long)frame * dfp + (long long)y * drp +
+          (long long)vx * NO;
+  const int nout = nvalid / F;
+#pragma unroll
+  for (int j = 0; j < NO; ++j)
+    if (j < nout) d[j] = (TD)acc[j];
+}
+
+template <typename TS, typename TD, int F>
+int launch_down_vec(const ssk_planes* p, const unsigned char* sr, const unsigned char* sd, unsigned char* r,
+                    unsigned char* d, long long drp, long long dfp, int ho, cudaStream_t st) {
+  constexpr int V = 16 / (int)sizeof(TS);
+  const int nvec = (p->w + V - 1) / V;
+  const dim3 grid((nvec + 127) / 128, ho, 2 * p->n);
+  box_down_vec_kernel<TS, TD, F><<<grid, 128, 0, st>>>(sr, sd, p->row_pitch, p->frame_pitch, p->w, r, d, drp, dfp,
+                                                       nvec);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+}
+
+template <typename TS, typename TD>
+int try_down_vec(const ssk_planes* p, int f, const unsigned char* sr, const unsigned char* sd, unsigned char* r,
+                 unsigned char* d, long long drp, long long dfp, int ho, cudaStream_t st) {
+  constexpr int V = 16 / (int)sizeof(TS);
+  const bool aligned = !((reinterpret_cast<uintptr_t>(sr) | reinterpret_cast<uintptr_t>(sd)) & 15) &&
+                       !((p->row_pitch * (long long)sizeof(TS)) & 15) && !((p->frame_pitch * (long long)sizeof(TS)) & 15);
+  if (!aligned || p->h % f || p->w % f) return 1;
+  switch (f) {
+    case 2: return launch_down_vec<TS, TD, 2>(p, sr, sd, r, d, drp, dfp, ho, st);
+    case 4: return V >= 4 ? launch_down_vec<TS, TD, (V >= 4 ? 4 : 1)>(p, sr, sd, r, d, drp, dfp, ho, st) : 1;
+    case 8: return V >= 8 ? launch_down_vec<TS, TD, (V >= 8 ? 8 : 1)>(p, sr, sd, r, d, drp, dfp, ho, st) : 1;
+    case 16: return V >= 16 ? launch_down_vec<TS, TD, (V >= 16 ? 16 : 1)>(p, sr, sd, r, d, drp, dfp, ho, st) : 1;
+    default: return 1;
+  }
+}
+
 template <typename TS>
 int launch_box_downsample_t(const ssk_planes* p, int f, void* dr, void* dd, int dst_dtype, long long drp,
                             long long dfp, int ho, int wo, cudaStream_t st) {
@@ -442,6 +575,13 @@ int launch_box_downsample_t(const ssk_planes* p, int f, void* dr, void* dd, int 
   const auto* sd = static_cast<const unsigned char*>(p->dist);
   auto* r = static_cast<unsigned char*>(dr);
   auto* d = static_cast<unsigned char*>(dd);
+  if constexpr (std::is_integral<TS>::value) {
+    if (dst_dtype == SSK_U16 || dst_dtype == SSK_U32) {
+      const int rc = dst_dtype == SSK_U16 ? try_down_vec<TS, uint16_t>(p, f, sr, sd, r, d, drp, dfp, ho, st)
+                                          : try_down_vec<TS, uint32_t>(p, f, sr, sd, r, d, drp, dfp, ho, st);
+      if (rc <= 0) return rc;  // launched (or failed); 1 = not eligible, use the generic kernel
+    }
+  }
   switch (dst_dtype) {
     case SSK_F64:
       box_downsample_kernel<TS, double><<<grid, 128, 0, st>>>(sr, sd, p->row_pitch, p->frame_pitch, p->h, p->w, f,
@@ -497,8 +637,9 @@ int plan_pool(const ssk_maps* m, const ssk_pooler* pl, PoolPlan& P) {
   a.w = m->w;
   const long long count = (long long)m->h * m->w;
   a.cnt = (double)count;
-  // ~16K samples per block, whole rows, geometry-only (independent of the batch)
-  long long nblk = (count + 16383) / 16384;
+  // one block per map up to 32K samples (single-launch small-map path), else ~16K
+  // samples per block; whole rows, geometry-only (independent of the batch)
+  long long nblk = count <= 32768 ? 1 : (count + 16383) / 16384;
   if (nblk > m->h) nblk = m->h;
   if (nblk > 1024) nblk = 1024;
   a.nblk = (int)(nblk < 1 ? 1 : nblk);
@@ -549,6 +690,11 @@ int plan_pool(const ssk_maps* m, const ssk_pooler* pl, PoolPlan& P) {
 template <typename T>
 int run_pool(PoolPlan& P, cudaStream_t st) {
   PoolArgs& a = P.a;
+  if (a.nblk == 1 && P.passes == 0) {
+    pool_small_kernel<T><<<a.n, PS_THREADS, 0, st>>>(a);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+  }
   const dim3 grid(a.nblk, a.n);
   pool_pass1_kernel<T><<<grid, PL_THREADS, 0, st>>>(a);
   note_launch();

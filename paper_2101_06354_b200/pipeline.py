@@ -148,11 +148,15 @@ def luma_records(pair: engine.DevicePair, config: SsimConfig, factor: Optional[i
 
 
 def score_batch(ref, dist, config: SsimConfig = SsimConfig(), stream=None) -> FrameRecords:
-    """Batched luma pipeline on [n, h, w] CUDA tensors: scaling + SSIM/MS-SSIM + spatial pooling."""
+    """Batched luma pipeline on [n, h, w] CUDA tensors: scaling + SSIM/MS-SSIM + spatial pooling.
+
+    Asynchronous (no host synchronisation); a zero-mean map under ``cov``
+    pooling yields NaN for that frame instead of raising ZeroMeanCoV.
+    """
     if config.color.model != "luma":
         raise ValidationError("score_batch scores luma planes; use color_batch for the channel-wise models")
     pair = engine.device_pair(ref, dist, config.bit_depth, config.window.shape == "gauss")
-    return luma_records(pair, config, stream=stream)
+    return luma_records(pair, config, stream=stream, strict=False)
 
 
 # ---------------------------------------------------------------------------
