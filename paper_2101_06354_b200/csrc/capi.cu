@@ -103,7 +103,14 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
     a.stride = s;
     // wide strips (256 V columns, 1 CTA/SM) for 8-bit frames under the warp-specialised
     // kernel: V-halo overhead 250/240 instead of 122/112 and fewer idle H threads
-    a.vcols = (gk::gauss_ws_level() >= 1 && p->dtype == SSK_U8 && k <= 17 && a.wo >= 480) ? 256 : 128;
+    // (u16 -- the scaled pyramid level 1 of 8-bit input -- only with SSK_WIDE_U16=1:
+    // measured no faster than the classic multi-level launch, which saves a launch)
+    static const int wide_u16 = [] {
+      const char* e = std::getenv("SSK_WIDE_U16");
+      return e ? std::atoi(e) : 0;
+    }();
+    const bool wide_ok = p->dtype == SSK_U8 || (p->dtype == SSK_U16 && wide_u16);
+    a.vcols = (gk::gauss_ws_level() >= 1 && wide_ok && k <= 17 && a.wo >= 480) ? 256 : 128;
     const int tw = gauss_tw(k, a.vcols);
     const int nstrips = (a.wo + tw - 1) / tw;
     // Segments depend on the frame geometry only (never on the batch size), so a
@@ -455,7 +462,7 @@ int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, const dou
     part_off += partial_bytes(plans[l], p->n);
   }
   for (int l = 0; l < levels;) {
-    if (l == 0 || !plans[l].gauss) {
+    if (l == 0 || !plans[l].gauss || plans[l].ga.vcols != GS_THREADS) {  // wide levels launch alone
       rc = run_plan(plans[l], const_cast<double*>(fa.partials[l]), nullptr, nullptr, st);
       if (rc) return rc;
       ++l;
@@ -463,7 +470,7 @@ int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, const dou
     }
     GaussLevels gl{};
     int ctas = 0;
-    while (l < levels && gl.nlev < GS_MAX_LEVELS && plans[l].gauss) {
+    while (l < levels && gl.nlev < GS_MAX_LEVELS && plans[l].gauss && plans[l].ga.vcols == GS_THREADS) {
       gl.lv[gl.nlev] = plans[l].ga;
       gl.cta_off[gl.nlev] = ctas;
       gl.nstrips[gl.nlev] = (int)plans[l].grid.x;

@@ -106,6 +106,8 @@ inline bool gauss_ws_enabled() { return gauss_ws_level() >= 1; }
 // groups hit 16 distinct 8-byte bank slots
 __host__ __device__ constexpr int vp_of(int vc) { return vc * 8 + 8; }
 __host__ __device__ constexpr int tw_of(int k, int vc) { return ((vc - (k - 1)) / 16) * 16; }
+// V tiles in flight: 3, except wide 16-bit strips (their doubled raw ring leaves room for 2)
+__host__ __device__ constexpr int nbuf_of(int vc, int es) { return (vc == 256 && es > 1) ? 2 : GS_NBUF; }
 
 // raw sample (as stored) -> float with the 2^23 splice for small integers
 template <typename TIN>
@@ -397,7 +399,8 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
     }
   } else {
     constexpr int VBYTES = NM * G * VP;
-    // GS_NBUF V tiles in flight; named barriers 2..2+NBUF-1 = "tile b full",
+    constexpr int NB = nbuf_of(VC, ES);
+    // NB V tiles in flight; named barriers 2..2+NB-1 = "tile b full",
     // 2+NBUF.. = "tile b free"; barrier 1 = producer-internal
     if (tid < VC) {  // producers
       int b = 0;
@@ -409,19 +412,19 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
           cp_async_wait<0>();
         }
         named_sync(1, VC);                                           // chunk c's raw rows visible
-        if (c >= GS_NBUF) named_sync(2 + GS_NBUF + b, 2 * VC);       // consumers released tile b
+        if (c >= NB) named_sync(2 + NB + b, 2 * VC);                 // consumers released tile b
         vpass(c, vbuf0 + b * VBYTES);
         named_arrive(2 + b, 2 * VC);                                 // tile b full
         named_sync(1, VC);                                           // raw rows of chunk c no longer read
-        b = b + 1 == GS_NBUF ? 0 : b + 1;
+        b = b + 1 == NB ? 0 : b + 1;
       }
     } else {  // consumers
       int b = 0;
       for (int c = 0; c < nchunks; ++c) {
         named_sync(2 + b, 2 * VC);
         hpass(c, vbuf0 + b * VBYTES);
-        if (c + GS_NBUF < nchunks) named_arrive(2 + GS_NBUF + b, 2 * VC);
-        b = b + 1 == GS_NBUF ? 0 : b + 1;
+        if (c + NB < nchunks) named_arrive(2 + NB + b, 2 * VC);
+        b = b + 1 == NB ? 0 : b + 1;
       }
     }
   }
@@ -479,7 +482,8 @@ inline size_t smem_bytes() {
 template <int K, typename TIN, int NM, int VC>
 int launch_ws(const GaussArgs& a, dim3 grid, cudaStream_t st) {
   auto fn = gauss_ws_kernel<K, TIN, NM, VC>;
-  const size_t smem = smem_bytes<K, TIN, NM, VC>() + (size_t)(GS_NBUF - 1) * NM * G * vp_of(VC);  // extra V tiles
+  const size_t smem = smem_bytes<K, TIN, NM, VC>() +
+                      (size_t)(nbuf_of(VC, (int)sizeof(TIN)) - 1) * NM * G * vp_of(VC);  // extra V tiles
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SSK_E_CUDA;
   fn<<<grid, 2 * VC, smem, st>>>(a);
@@ -490,7 +494,7 @@ int launch_ws(const GaussArgs& a, dim3 grid, cudaStream_t st) {
 template <int K, typename TIN, int NM>
 int launch_nm(const GaussArgs& a, dim3 grid, cudaStream_t st) {
   if (NM == 4 && a.vcols == 256) {
-    if constexpr (sizeof(TIN) == 1 && 256 - (K - 1) >= 16) return launch_ws<K, TIN, NM, 256>(a, grid, st);
+    if constexpr (sizeof(TIN) <= 2 && 256 - (K - 1) >= 16) return launch_ws<K, TIN, NM, 256>(a, grid, st);
     return SSK_E_ARG;
   }
   if (NM == 4 && gauss_ws_enabled()) return launch_ws<K, TIN, NM, GS_THREADS>(a, grid, st);
