@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SSK_ABI_VERSION 5
+#define SSK_ABI_VERSION 6
 
 /* sample storage types */
 enum {
@@ -260,6 +260,53 @@ size_t ssk_pool_workspace_bytes(const ssk_maps* m, const ssk_pooler* pool);
 /* d_out [n] pooled scores; d_mean [n] (nullable) the plain mean of each map. */
 int ssk_pool_spatial(const ssk_maps* m, const ssk_pooler* pool, double* d_out, double* d_mean,
                      void* d_workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Colorimetric models (src/color.py:27-371): qssim, cmssim, hssim and the
+ * conversions they need.  A color frame batch is three device planes per
+ * frame; 4:2:0 chroma planes are ceil(h/2) x ceil(w/2) and are upsampled by
+ * nearest neighbour (upsample_chroma, :92-101) where a model needs co-sited
+ * channels.
+ */
+enum { SSK_SPACE_RGB = 1, SSK_SPACE_YCBCR = 2 };
+enum {
+  SSK_CONV_RGB = 1,       /* -> R, G, B (YCbCr input: inverse BT.709, clamped, :76-89)   */
+  SSK_CONV_YCBCR = 2,     /* -> Y, Cb, Cr 4:4:4 (RGB input: forward BT.709, :64-73)      */
+  SSK_CONV_LUMA = 3,      /* -> luma_of (:104-108)                                       */
+  SSK_CONV_HUE = 4,       /* -> hue_plane scaled to [0, L] (:341-362)                     */
+  SSK_CONV_LAB_EMBED = 5  /* -> CIELAB * L/100, qssim's 'lab' embedding (:172-178)        */
+};
+
+typedef struct ssk_color {
+  const void* ch[3];           /* device planes (R,G,B or Y,Cb,Cr)                     */
+  int32_t dtype;               /* SSK_U8 / SSK_U16 / SSK_F32 / SSK_F64                  */
+  int32_t space;               /* SSK_SPACE_RGB / SSK_SPACE_YCBCR                       */
+  int32_t subsampling;         /* 0 = 4:4:4, 1 = 4:2:0 (YCbCr only)                     */
+  int32_t n, h, w;             /* frames, luma rows, luma columns                       */
+  int32_t bit_depth;           /* L = 2^bit_depth - 1                                   */
+  int64_t row_pitch[3];        /* elements, per channel                                 */
+  int64_t frame_pitch[3];
+} ssk_color;
+
+/* float64 planes out: d_out[f * out_frame_pitch + plane * h * out_row_pitch + y * out_row_pitch + x]. */
+int ssk_color_convert(const ssk_color* src, int op, double* d_out, int64_t out_row_pitch, int64_t out_frame_pitch,
+                      void* stream);
+
+/* Quaternion SSIM (qssim, :181-256) of two float64 embeddings [n][3][h][row_pitch]
+ * (frame_pitch elements between frames), rect k x k window, stride; d_means [n]. */
+size_t ssk_qssim_workspace_bytes(int n, int h, int w, int k, int stride);
+int ssk_qssim(const double* d_emb_ref, const double* d_emb_dist, int n, int h, int w, int64_t row_pitch,
+              int64_t frame_pitch, int k, int stride, double c1, double c2, double* d_means, void* d_workspace,
+              size_t workspace_bytes, void* stream);
+
+/* CIELAB difference (delta_e_map, :290-296; smooth = opponent-space chroma
+ * smoothing) sampled at the centres of the k/stride window grid:
+ * d_out [n][gh][gw]; mode 0 = dE, mode 1 = 1 - dE/45 (cmssim's weight before
+ * the clamp to [0, 1], :299-334).  k = stride = 1 gives the full map. */
+size_t ssk_delta_e_workspace_bytes(int n, int h, int w);
+int ssk_delta_e(const ssk_color* ref, const ssk_color* dist, int smooth, int k, int stride, int mode, double* d_out,
+                int64_t out_row_pitch, int64_t out_frame_pitch, void* d_workspace, size_t workspace_bytes,
+                void* stream);
 
 /* Number of kernels this library has launched since load (for bench.py). */
 uint64_t ssk_launch_count(void);

@@ -20,6 +20,10 @@ order, so that its outputs are bit-identical to the reference's:
   box_downsample ......... src/adaptation.py:93-110     (block means, ragged edges)
   pool_spatial ........... src/pooling.py:157-243       (am cov md fns dw mink lw pp)
   luma_frame_record ...... src/pipeline.py:197-236      (scale -> stats -> pool record)
+  color conversions ...... src/color.py:64-108          (BT.709 YCbCr, luma, 4:2:0 upsample)
+  qssim .................. src/color.py:159-256         (quaternion windowed similarity)
+  delta_e / cmssim ....... src/color.py:263-334         (opponent smoothing, CIELAB weights)
+  hue / hssim ............ src/color.py:341-371
 
 Parity pinning: tests/test_oracle_golden.py checks this module against
 golden vectors produced by the reference itself (tests/golden/make_golden.py,
@@ -400,3 +404,160 @@ def luma_frame_record(ref, dist, shape: str = "rect", k: int = 11, stride: int =
     l_map, cs_map, q = term_maps(*stats, c1, c2)
     score = pool_spatial(q, pool, ref_luma=stats[0], **pool_params)
     return score, float(q.mean()), float(l_map.mean()), float(cs_map.mean())
+
+
+# ---------------------------------------------------------------------------
+# colorimetric models (src/color.py:27-371)
+# ---------------------------------------------------------------------------
+
+KR, KG, KB = 0.213, 0.715, 0.072
+CB_SCALE, CR_SCALE = 0.539, 0.635
+RGB_TO_XYZ = np.array([[0.4124564, 0.3575761, 0.1804375],
+                       [0.2126729, 0.7151522, 0.0721750],
+                       [0.0193339, 0.1191920, 0.9503041]])
+D65 = (0.95047, 1.0, 1.08883)
+XYZ_TO_Q = np.array([[0.279, 0.72, -0.107], [-0.449, 0.29, -0.077], [0.086, -0.59, 0.501]])
+Q_TO_XYZ = np.array([[0.6204, -1.8704, -0.1553], [1.3661, 0.9316, 0.4339], [1.5013, 1.4176, 2.5331]])
+DELTA_E_FULL_MASK = 45.0
+
+
+def _f64(chans):
+    return [np.asarray(c, dtype=np.float64) for c in chans]
+
+
+def upsample420(chans, h: int, w: int):
+    """Nearest-neighbour chroma upsampling to the luma grid."""
+    y, cb, cr = chans
+    return [y] + [np.repeat(np.repeat(c, 2, axis=0), 2, axis=1)[:h, :w] for c in (cb, cr)]
+
+
+def rgb_to_ycbcr(chans, peak: float):
+    r, g, b = _f64(chans)
+    y = KR * r + KG * g + KB * b
+    half = peak / 2.0
+    return [y, CB_SCALE * (b - y) + half, CR_SCALE * (r - y) + half]
+
+
+def ycbcr_to_rgb(chans, peak: float):
+    """Inverse BT.709 of 4:4:4 channels, clamped to [0, peak]."""
+    y, cb, cr = _f64(chans)
+    half = peak / 2.0
+    b = (cb - half) / CB_SCALE + y
+    r = (cr - half) / CR_SCALE + y
+    g = (y - KR * r - KB * b) / KG
+    return [np.clip(c, 0.0, peak) for c in (r, g, b)]
+
+
+def luma_rgb(chans):
+    r, g, b = _f64(chans)
+    return KR * r + KG * g + KB * b
+
+
+def hue(chans, peak: float):
+    """HSV hue scaled to [0, peak]; achromatic pixels 0."""
+    r, g, b = _f64(chans)
+    hi = np.maximum(np.maximum(r, g), b)
+    lo = np.minimum(np.minimum(r, g), b)
+    d = hi - lo
+    safe = np.where(d == 0.0, 1.0, d)
+    h = np.where(d == 0.0, 0.0,
+                 np.where(hi == r, np.mod((g - b) / safe, 6.0),
+                          np.where(hi == g, (b - r) / safe + 2.0, (r - g) / safe + 4.0)))
+    h = h * 60.0
+    return h / 360.0 * peak
+
+
+def smooth_reflect(values, sigma: float = 2.0, k: int = 13):
+    """Separable Gaussian, reflect padding, same-size output."""
+    g = gaussian_kernel(sigma, k)[(k - 1) // 2]
+    g = g / g.sum()
+    pad = (k - 1) // 2
+    v = np.pad(values, ((pad, pad), (0, 0)), mode="reflect")
+    v = sum(g[m] * v[m:m + values.shape[0], :] for m in range(k))
+    v = np.pad(v, ((0, 0), (pad, pad)), mode="reflect")
+    return sum(g[n] * v[:, n:n + values.shape[1]] for n in range(k))
+
+
+def rgb_to_lab(chans, peak: float, smooth: bool = False):
+    rgb = np.stack([np.asarray(c, dtype=np.float64) / peak for c in chans])
+    xyz = RGB_TO_XYZ @ rgb.reshape(3, -1)
+    if smooth:
+        q = (XYZ_TO_Q @ xyz).reshape(3, *rgb.shape[1:])
+        q = np.stack([q[0], smooth_reflect(q[1]), smooth_reflect(q[2])])
+        xyz = Q_TO_XYZ @ q.reshape(3, -1)
+    x, y, z = (c.reshape(rgb.shape[1:]) for c in xyz)
+
+    def f(t):
+        d = 6.0 / 29.0
+        return np.where(t > d ** 3, np.cbrt(t), t / (3 * d * d) + 4.0 / 29.0)
+
+    fx, fy, fz = f(x / D65[0]), f(y / D65[1]), f(z / D65[2])
+    return [116.0 * fy - 16.0, 500.0 * (fx - fy), 200.0 * (fy - fz)]
+
+
+def delta_e(rgb1, rgb2, peak: float, smooth: bool = True):
+    l1, l2 = rgb_to_lab(rgb1, peak, smooth), rgb_to_lab(rgb2, peak, smooth)
+    return np.sqrt(sum((a - b) ** 2 for a, b in zip(l1, l2)))
+
+
+def qssim(emb1, emb2, k: int, stride: int, peak: float, k1: float = 0.01, k2: float = 0.03) -> float:
+    """Quaternion SSIM of two 3-channel embeddings (pure quaternions on i, j, k)."""
+    r1, g1, b1 = _f64(emb1)
+    r2, g2, b2 = _f64(emb2)
+    c1, c2 = (k1 * peak) ** 2, (k2 * peak) ** 2
+    kern = np.full((k, k), 1.0 / (k * k))
+
+    def wm(x):
+        return sliding_sums(x, kern, k, stride)
+
+    m1 = [wm(r1), wm(g1), wm(b1)]
+    m2 = [wm(r2), wm(g2), wm(b2)]
+    e_dot = wm(r1 * r2 + g1 * g2 + b1 * b2)
+    e_i = wm(-(g1 * b2 - b1 * g2))
+    e_j = wm(-(b1 * r2 - r1 * b2))
+    e_k = wm(-(r1 * g2 - g1 * r2))
+    e_sq1 = wm(r1 * r1 + g1 * g1 + b1 * b1)
+    e_sq2 = wm(r2 * r2 + g2 * g2 + b2 * b2)
+    mdot = m1[0] * m2[0] + m1[1] * m2[1] + m1[2] * m2[2]
+    mi = -(m1[1] * m2[2] - m1[2] * m2[1])
+    mj = -(m1[2] * m2[0] - m1[0] * m2[2])
+    mk = -(m1[0] * m2[1] - m1[1] * m2[0])
+    n1 = m1[0] ** 2 + m1[1] ** 2 + m1[2] ** 2
+    n2 = m2[0] ** 2 + m2[1] ** 2 + m2[2] ** 2
+    num1 = np.sqrt((2.0 * mdot + c1) ** 2 + (2.0 * mi) ** 2 + (2.0 * mj) ** 2 + (2.0 * mk) ** 2)
+    num2 = np.sqrt((2.0 * (e_dot - mdot) + c2) ** 2 + (2.0 * (e_i - mi)) ** 2 + (2.0 * (e_j - mj)) ** 2
+                   + (2.0 * (e_k - mk)) ** 2)
+    den1 = n1 + n2 + c1
+    den2 = (e_sq1 - n1) + (e_sq2 - n2) + c2
+    return float(((num1 / den1) * (num2 / den2)).mean())
+
+
+def qssim_embedding(chans, space: str, peak: float, ycc: bool = False, h: int = 0, w: int = 0):
+    """Embedding channels: rgb as is, BT.709 YCbCr (converted from RGB or upsampled 4:2:0), Lab * peak/100."""
+    if ycc:
+        chans = upsample420(chans, h, w)
+        if space == "ycbcr":
+            return _f64(chans)
+        chans = ycbcr_to_rgb(chans, peak)
+    if space == "rgb":
+        return _f64(chans)
+    if space == "ycbcr":
+        return rgb_to_ycbcr(chans, peak)
+    return [c * (peak / 100.0) for c in rgb_to_lab(chans, peak)]
+
+
+def cmssim(rgb1, rgb2, peak: float, bit_depth: int, **window) -> float:
+    """Luma SSIM map weighted by clamp(1 - dE/45, 0, 1) sampled at window centres."""
+    _, _, q = ssim_maps(luma_rgb(rgb1), luma_rgb(rgb2), bit_depth=bit_depth, **window)
+    wgt = np.clip(1.0 - delta_e(rgb1, rgb2, peak, True) / DELTA_E_FULL_MASK, 0.0, 1.0)
+    k, s = window["k"], window.get("stride", 1)
+    c = (k - 1) // 2
+    rows = np.arange(q.shape[0]) * s + c
+    cols = np.arange(q.shape[1]) * s + c
+    return float((q * wgt[np.ix_(rows, cols)]).mean())
+
+
+def hssim(rgb1, rgb2, peak: float, bit_depth: int, **window) -> float:
+    luma = ssim_maps(luma_rgb(rgb1), luma_rgb(rgb2), bit_depth=bit_depth, **window)[2].mean()
+    hue_s = ssim_maps(hue(rgb1, peak), hue(rgb2, peak), bit_depth=bit_depth, **window)[2].mean()
+    return float((luma + 0.2 * hue_s) / 1.2)

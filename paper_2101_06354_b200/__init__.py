@@ -23,6 +23,7 @@ from .chroma import (
     upsample_chroma,
     ycbcr_bt709_to_rgb,
 )
+from .colorimetric import cmssim, delta_e_map, hssim, hue_plane, qssim
 from .errors import SsimkitError
 from .moments import (
     IntegralSet,
@@ -92,6 +93,7 @@ __all__ = [
     # color
     "channel_scores", "channelwise_cssim", "combine_channelwise", "fixed_weight_cssim", "luma_of",
     "rgb_to_ycbcr_bt709", "upsample_chroma", "ycbcr_bt709_to_rgb",
+    "cmssim", "delta_e_map", "hssim", "hue_plane", "qssim",
     # pooling
     "SpatialPooler", "TemporalPooler", "parse_spatial", "parse_temporal", "pool_maps", "pool_spatial",
     "pool_temporal",

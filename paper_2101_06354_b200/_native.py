@@ -32,7 +32,7 @@ RECT, GAUSS = 1, 2
 WANT_Q, WANT_L, WANT_CS, MAP_TERMS, MAP_STATS = 1, 2, 4, 8, 16
 E_ARG, E_WINDOW, E_SHAPE, E_WORKSPACE, E_ALIGN, E_CUDA, E_LEVELS, E_TOO_SMALL = range(-1, -9, -1)
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 EXPORTED_SYMBOLS = (
     "ssk_abi_version",
@@ -51,9 +51,17 @@ EXPORTED_SYMBOLS = (
     "ssk_box_downsample",
     "ssk_pool_workspace_bytes",
     "ssk_pool_spatial",
+    "ssk_color_convert",
+    "ssk_qssim_workspace_bytes",
+    "ssk_qssim",
+    "ssk_delta_e_workspace_bytes",
+    "ssk_delta_e",
     "ssk_launch_count",
     "ssk_probe_fp32_tflops",
 )
+
+SPACE_RGB, SPACE_YCBCR = 1, 2
+CONV_RGB, CONV_YCBCR, CONV_LUMA, CONV_HUE, CONV_LAB_EMBED = 1, 2, 3, 4, 5
 
 # spatial pooler kinds (SSK_POOL_*), in SPATIAL_KINDS order of src/pooling.py:29
 POOL_KINDS = {"am": 0, "cov": 1, "md": 2, "fns": 3, "dw": 4, "mink": 5, "lw": 6, "pp": 7}
@@ -110,6 +118,21 @@ class Pooler(ctypes.Structure):
         ("b", ctypes.c_double),
         ("ps", ctypes.c_double),
         ("rs", ctypes.c_double),
+    ]
+
+
+class Color(ctypes.Structure):
+    _fields_ = [
+        ("ch", ctypes.c_void_p * 3),
+        ("dtype", ctypes.c_int32),
+        ("space", ctypes.c_int32),
+        ("subsampling", ctypes.c_int32),
+        ("n", ctypes.c_int32),
+        ("h", ctypes.c_int32),
+        ("w", ctypes.c_int32),
+        ("bit_depth", ctypes.c_int32),
+        ("row_pitch", ctypes.c_int64 * 3),
+        ("frame_pitch", ctypes.c_int64 * 3),
     ]
 
 
@@ -175,6 +198,19 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         lib.ssk_pool_workspace_bytes.argtypes = [pM, pQ]
         lib.ssk_pool_spatial.restype = i32
         lib.ssk_pool_spatial.argtypes = [pM, pQ, vp, vp, vp, sz, vp]
+        pC, pD = ctypes.POINTER(Color), ctypes.POINTER(ctypes.c_double)
+        lib.ssk_color_convert.restype = i32
+        lib.ssk_color_convert.argtypes = [pC, i32, vp, i64, i64, vp]
+        lib.ssk_qssim_workspace_bytes.restype = sz
+        lib.ssk_qssim_workspace_bytes.argtypes = [i32, i32, i32, i32, i32]
+        lib.ssk_qssim.restype = i32
+        lib.ssk_qssim.argtypes = [vp, vp, i32, i32, i32, i64, i64, i32, i32, ctypes.c_double, ctypes.c_double, vp,
+                                  vp, sz, vp]
+        lib.ssk_delta_e_workspace_bytes.restype = sz
+        lib.ssk_delta_e_workspace_bytes.argtypes = [i32, i32, i32]
+        lib.ssk_delta_e.restype = i32
+        lib.ssk_delta_e.argtypes = [pC, pC, i32, i32, i32, i32, vp, i64, i64, vp, sz, vp]
+        del pD
         lib.ssk_launch_count.restype = ctypes.c_uint64
         lib.ssk_probe_fp32_tflops.restype = i32
         lib.ssk_probe_fp32_tflops.argtypes = [ctypes.c_double, ctypes.POINTER(ctypes.c_double), vp]

@@ -4,9 +4,8 @@ Each channel is scored at its own resolution (4:2:0 chroma is not
 upsampled, src/color.py:122-125, :144-153) by the fused SSIM kernel; only the
 three per-channel means return to the host, where they are combined in
 float64 with the reference's formulas.  The BT.709 conversions needed to
-accept RGB input are plain per-pixel float64 maps kept here for API parity
-(src/color.py:64-108); the quaternion / CIELAB / hue models are outside the
-accelerated path.
+accept RGB input run on the device (``colorimetric.py``, src/color.py:64-108),
+as do the quaternion / CIELAB / hue models.
 """
 
 from __future__ import annotations
@@ -15,53 +14,19 @@ import numpy as np
 
 from .errors import DegenerateWeights, ValidationError, WrongSpace
 from .options import SsimConfig
-from .planes import CHROMA_444, SPACE_RGB, SPACE_YCBCR, ColorFrame, LumaPlane, validate_color_pair
+from .planes import CHROMA_444, SPACE_RGB, SPACE_YCBCR, ColorFrame, validate_color_pair
 from .scoring import ssim_score
 
-_KR, _KG, _KB = 0.213, 0.715, 0.072
-_CB_SCALE, _CR_SCALE = 0.539, 0.635
-
-
-def rgb_to_ycbcr_bt709(frame: ColorFrame) -> ColorFrame:
-    """BT.709 RGB -> YCbCr, chroma offset by L/2 (src/color.py:64-73)."""
-    frame.require_space(SPACE_RGB)
-    r, g, b = (np.asarray(c, dtype=np.float64) for c in frame.channels)
-    half = frame.peak / 2.0
-    y = _KR * r + _KG * g + _KB * b
-    return ColorFrame((y, _CB_SCALE * (b - y) + half, _CR_SCALE * (r - y) + half), SPACE_YCBCR,
-                      frame.subsampling, frame.bit_depth)
+from .colorimetric import luma_of, rgb_to_ycbcr_bt709, ycbcr_bt709_to_rgb  # noqa: F401  (device conversions)
 
 
 def upsample_chroma(frame: ColorFrame) -> ColorFrame:
-    """Nearest-neighbour 4:2:0 -> 4:4:4 (src/color.py:92-101)."""
+    """Nearest-neighbour 4:2:0 -> 4:4:4 (src/color.py:92-101): pure sample replication."""
     if frame.subsampling == CHROMA_444:
         return frame
     h, w = frame.height, frame.width
     up = [np.repeat(np.repeat(c, 2, axis=0), 2, axis=1)[:h, :w] for c in frame.channels[1:]]
     return ColorFrame((frame.channels[0], up[0], up[1]), frame.space, CHROMA_444, frame.bit_depth)
-
-
-def ycbcr_bt709_to_rgb(frame: ColorFrame) -> ColorFrame:
-    """Inverse BT.709 (4:4:4), clamped to the nominal range (src/color.py:76-89)."""
-    frame.require_space(SPACE_YCBCR)
-    frame = upsample_chroma(frame)
-    y, cb, cr = (np.asarray(c, dtype=np.float64) for c in frame.channels)
-    half = frame.peak / 2.0
-    b = (cb - half) / _CB_SCALE + y
-    r = (cr - half) / _CR_SCALE + y
-    g = (y - _KR * r - _KB * b) / _KG
-    return ColorFrame(tuple(np.clip(c, 0.0, frame.peak) for c in (r, g, b)), SPACE_RGB, CHROMA_444,
-                      frame.bit_depth)
-
-
-def luma_of(frame: ColorFrame) -> LumaPlane:
-    """Luminance plane of an RGB or YCbCr frame (src/color.py:104-108)."""
-    if frame.space == SPACE_YCBCR:
-        return LumaPlane(frame.channels[0], frame.bit_depth)
-    if frame.space == SPACE_RGB:
-        r, g, b = (np.asarray(c, dtype=np.float64) for c in frame.channels)
-        return LumaPlane(_KR * r + _KG * g + _KB * b, frame.bit_depth)
-    raise WrongSpace(f"no luminance definition for {frame.space} frames")
 
 
 def combine_channelwise(fy: float, fcb: float, fcr: float, alpha: float, beta: float) -> float:

@@ -180,9 +180,8 @@ def score_frame_pair(ref, dist, config: SsimConfig, volume=None) -> FrameScore:
 
     Luma model: resolution adaptation, SSIM with the configured spatial pooler
     or MS-SSIM (score only), or SSIM-3D when a ``RollingVolume`` is given.
-    Channel-wise color models ``cw`` / ``fixed`` on YCbCr/RGB frames.  The
-    qssim / cmssim / hssim models are outside the accelerated path (SURVEY.md
-    §8(f) rank 4) and raise ``ValidationError``.
+    Color models ``cw`` / ``fixed`` (channel-wise) and ``qssim`` / ``cmssim`` /
+    ``hssim`` (colorimetric, ``colorimetric.py``) on YCbCr/RGB frames.
     """
     from . import chroma
     from .planes import ColorFrame, plane_bit_depth, plane_data, validate_color_pair, validate_frame_pair
@@ -214,7 +213,18 @@ def score_frame_pair(ref, dist, config: SsimConfig, volume=None) -> FrameScore:
         return FrameScore(chroma.channelwise_cssim(ref, dist, cfg.color.alpha, cfg.color.beta, cfg), None, None, None)
     if model == "fixed":
         return FrameScore(chroma.fixed_weight_cssim(ref, dist, cfg.color.weights, cfg), None, None, None)
-    raise ValidationError(f"color model {model!r} is not part of the accelerated path")
+    from . import colorimetric as cm
+
+    if model == "qssim":
+        pair = (ref, dist)
+        if cfg.color.space in ("rgb", "lab") and ref.space != "rgb":
+            pair = (cm.ycbcr_bt709_to_rgb(ref), cm.ycbcr_bt709_to_rgb(dist))
+        score = cm.qssim(*pair, window=cfg.window, k1=cfg.k1, k2=cfg.k2, space=cfg.color.space)
+    elif model == "cmssim":
+        score = cm.cmssim(ref, dist, cfg.window, cfg)
+    else:  # hssim
+        score = cm.hssim(ref, dist, cfg.window, cfg)
+    return FrameScore(score, None, None, None)
 
 
 def _volume_score(volume, y1, y2, cfg: SsimConfig) -> FrameScore:
