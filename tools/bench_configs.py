@@ -95,6 +95,21 @@ def main() -> None:
                        "path": "score_batch(enhanced preset): box downsample x4 -> rect11/s5 maps -> device CoV"}
     del ref, dist
 
+    # colorimetric models: per-pair API at 1080p RGB (host frames in, score out)
+    rng = np.random.default_rng(77)
+    rgb_r = tuple(synth.inv_f_noise(rng, 1080, 1920, 255.0).astype(np.uint8) for _ in range(3))
+    rgb_d = tuple(np.clip(c.astype(np.int16) + rng.integers(-8, 9, c.shape), 0, 255).astype(np.uint8) for c in rgb_r)
+    fr, fd = P.ColorFrame(rgb_r), P.ColorFrame(rgb_d)
+    for name, fn in (("qssim", lambda: P.qssim(fr, fd)), ("cmssim", lambda: P.cmssim(fr, fd)),
+                     ("hssim", lambda: P.hssim(fr, fd))):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(5):
+            v = fn()
+        dt = (time.perf_counter() - t0) / 5
+        out[name] = {"ms_per_pair": dt * 1e3, "score": v, "path": f"{name}(ColorFrame 1080p RGB u8), rect 11"}
+
     # config 3: YUV420 video through the frame-stream API (host frames -> pinned ring -> GPU)
     nfr = 300
     vid = synth.VideoConfig3(frames=nfr)
