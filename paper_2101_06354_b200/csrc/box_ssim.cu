@@ -88,7 +88,7 @@ __device__ __forceinline__ T load_sample(const unsigned char* p) {
 // MOM = true: the five per-pixel moments come precomputed from int64 planes
 // (the rolling temporal sums of a RollingVolume, src/spatiotemporal.py:60-138)
 // instead of being formed from staged x / y samples; everything else is shared.
-template <typename TIN, typename ACC, bool MOM = false>
+template <typename TIN, typename ACC, bool MOM = false, bool FAST = false>
 __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_constant__ BoxArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double s_red[(BX_THREADS / 32) * 3];
@@ -223,6 +223,11 @@ __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_consta
 #pragma unroll
         for (int m = 0; m < 5; ++m) ws[m * a.map_plane] = (long long)sums[m];
       }
+      if constexpr (FAST) {
+        box_fast_terms(a, (unsigned long long)sums[0], (unsigned long long)sums[1], (unsigned long long)sums[2],
+                       (unsigned long long)sums[3], (unsigned long long)sums[4], sq, sl, scs);
+        continue;
+      }
       const BoxTerms t = box_terms(__dmul_rn((double)sums[0], a.sscale1),
                                    __dmul_rn((double)sums[1], a.sscale1),
                                    __dmul_rn((double)sums[2], a.sscale2),
@@ -298,7 +303,8 @@ size_t box_smem_bytes(const BoxArgs& a, bool wide) {
 
 template <typename TIN, typename ACC>
 static int launch_int_t(const BoxArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
-  auto fn = box_int_kernel<TIN, ACC>;
+  const bool fast = !(a.want & (SSK_MAP_TERMS | SSK_MAP_STATS)) && !a.wsums && a.fast_ok;
+  auto fn = fast ? box_int_kernel<TIN, ACC, false, true> : box_int_kernel<TIN, ACC, false, false>;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SSK_E_CUDA;
   fn<<<grid, BX_THREADS, smem, st>>>(a);

@@ -157,6 +157,12 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
   a.sscale1 = std::ldexp(1.0, -p->scale_log2);
   a.sscale2 = std::ldexp(1.0, -2 * p->scale_log2);
   a.area = (double)k * (double)k;
+  a.area_i = k * k;
+  a.c1i = (float)(win->c1 * a.area * a.area * std::ldexp(1.0, 2 * p->scale_log2));
+  a.c2i = (float)(win->c2 * a.area * a.area * std::ldexp(1.0, 2 * p->scale_log2));
+  a.c1d = win->c1 * a.area * a.area * std::ldexp(1.0, 2 * p->scale_log2);
+  a.c2d = win->c2 * a.area * a.area * std::ldexp(1.0, 2 * p->scale_log2);
+  a.fast_ok = (a.area * a.area * stored_max * stored_max < 4.0e15) ? 1 : 0;
   int ex = 0;
   const double fr = std::frexp(a.area, &ex);
   a.area_pow2 = (fr == 0.5) ? 1 : 0;

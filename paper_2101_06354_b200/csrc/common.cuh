@@ -64,6 +64,40 @@ __device__ __forceinline__ void block_sum_store(double (&v)[NV], double* scratch
   }
 }
 
+// Reciprocal from the MUFU seed refined by two Newton steps (~1 ulp).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Score-only epilogue of the rect-window kernels (no maps and no integer sums
+// requested).  The window moments stay exact integers -- k^2 var = k^2 Q - S^2
+// (>= 0) and k^2 cov = k^2 P - S1 S2 in 64-bit, exactly representable in
+// float64 below 2^53 (BoxArgs::fast_ok) -- so no cancellation is left, and
+//   l  = (2 S1 S2 + C1')           / (S1^2 + S2^2 + C1')
+//   cs = (2 (k^2 P - S1 S2) + C2') / ((k^2 Q1 - S1^2) + (k^2 Q2 - S2^2) + C2'),
+// C' = C k^4 4^scale, each with one rounded add and a Newton reciprocal:
+// scores agree with the reference's float64 expression to ~1e-15.  Maps keep
+// the reference's own operation order (bit-identical) and never come here.
+template <typename Args>
+__device__ __forceinline__ void box_fast_terms(const Args& a, unsigned long long s1, unsigned long long s2,
+                                               unsigned long long q1, unsigned long long q2, unsigned long long p,
+                                               double& sq, double& sl, double& scs) {
+  const unsigned long long A = (unsigned long long)a.area_i;
+  const unsigned long long p11 = s1 * s1, p22 = s2 * s2, p12 = s1 * s2;
+  const unsigned long long v12 = (A * q1 - p11) + (A * q2 - p22);
+  const long long cv2 = 2 * ((long long)(A * p) - (long long)p12);
+  const double l = __dmul_rn(__dadd_rn((double)(2 * p12), a.c1d), rcp_nr(__dadd_rn((double)(p11 + p22), a.c1d)));
+  const double cs = __dmul_rn(__dadd_rn((double)cv2, a.c2d), rcp_nr(__dadd_rn((double)v12, a.c2d)));
+  sq += __dmul_rn(l, cs);
+  sl += l;
+  scs += cs;
+}
+
 // Number of kernels launched by this library (bench.py's gpu_launches claim).
 void note_launch(int count = 1);
 

@@ -68,6 +68,10 @@ struct BoxArgs {
   int in_pitch;               // staging row pitch, bytes
   int nslot;                  // prefix history slots
   double sscale1, sscale2;    // 2^-scale_log2, 2^-2*scale_log2 (exact rescaling of sums)
+  float c1i, c2i;             // C * area^2 * 4^scale_log2: constants of the integer-domain score epilogue
+  double c1d, c2d;
+  int fast_ok;                // area^2 * stored_max^2 < 2^52: the integer-domain epilogue is exact in u64/f64
+  int area_i;                 // k * k
   double area, inv_area;
   int area_pow2;              // area is a power of two: x/area == x*inv_area exactly
   double c1, c2;
