@@ -26,6 +26,14 @@ int gauss_ws_level() {
 }  // namespace gk
 
 static std::atomic<unsigned long long> g_launches{0};
+// SSK_FUSED_L1=0 restores the separate pyramid pass for level 1 (A/B switch)
+static int fused_l1_enabled() {
+  static const int v = [] {
+    const char* e = std::getenv("SSK_FUSED_L1");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
 void note_launch(int count) { g_launches.fetch_add((unsigned long long)count); }
 int probe_fp32(double seconds, double* tflops, cudaStream_t st);
 
@@ -118,6 +126,7 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
     // however frames are batched or sharded.
     int nseg = (a.ho + 127) / 128;
     a.seg_rows = (a.ho + nseg - 1) / nseg;
+    if (a.vcols == 256) a.seg_rows += a.seg_rows & 1;  // even: segments own whole 2x2 pyramid blocks
     nseg = (a.ho + a.seg_rows - 1) / a.seg_rows;
     const float shift = (float)std::ldexp(1.0, p->bit_depth - 1);
     const double scale = std::ldexp(1.0, -p->scale_log2);
@@ -418,30 +427,7 @@ int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, const dou
     lv[l].planes.dist = ws + lv[l].offset_d;
   }
 
-  // 1) the pyramid: up to four levels per pass over the previous top level
-  for (int base = 0; base + 1 < levels;) {
-    const int nl = std::min(GS_MAX_LEVELS, levels - 1 - base);
-    const ssk_planes& s = lv[base].planes;
-    PyramidArgs pa{};
-    pa.src_r = static_cast<const unsigned char*>(s.ref);
-    pa.src_d = static_cast<const unsigned char*>(s.dist);
-    pa.src_rp = s.row_pitch;
-    pa.src_fp = s.frame_pitch;
-    for (int i = 0; i < nl; ++i) {
-      const ssk_planes& d = lv[base + 1 + i].planes;
-      pa.dst_r[i] = const_cast<unsigned char*>(static_cast<const unsigned char*>(d.ref));
-      pa.dst_d[i] = const_cast<unsigned char*>(static_cast<const unsigned char*>(d.dist));
-      pa.dst_rp[i] = d.row_pitch;
-      pa.dst_fp[i] = d.frame_pitch;
-      pa.hl[i] = d.h;
-      pa.wl[i] = d.w;
-    }
-    rc = launch_pyramid(pa, s.dtype, lv[base + 1].planes.dtype, nl, p->n, st);
-    if (rc) return rc;
-    base += nl;
-  }
-
-  // 2) SSIM per level: level 0 alone (input type), the coarser levels batched
+  // per-level plans (the pyramid levels' geometry is known before any launch)
   FinalizeArgs fa{};
   fa.levels = levels;
   fa.n = p->n;
@@ -467,7 +453,49 @@ int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, const dou
     }
     part_off += partial_bytes(plans[l], p->n);
   }
-  for (int l = 0; l < levels;) {
+
+  // level 1 fused into the level-0 pass: the wide warp-specialised u8 kernel's producers
+  // write the 2x2 sums of the rows they stage anyway (one HBM read of level 0 less)
+  const bool fuse_l1 = levels >= 2 && plans[0].gauss && plans[0].ga.vcols == 256 && p->dtype == SSK_U8 &&
+                       lv[1].planes.dtype == SSK_U16 && fused_l1_enabled();
+  if (fuse_l1) {
+    GaussArgs& g0 = plans[0].ga;
+    g0.l1_ref = static_cast<unsigned short*>(const_cast<void*>(lv[1].planes.ref));
+    g0.l1_dist = static_cast<unsigned short*>(const_cast<void*>(lv[1].planes.dist));
+    g0.l1_rp = lv[1].planes.row_pitch;
+    g0.l1_fp = lv[1].planes.frame_pitch;
+    g0.l1_h = lv[1].planes.h;
+    g0.l1_w = lv[1].planes.w;
+    rc = run_plan(plans[0], const_cast<double*>(fa.partials[0]), nullptr, nullptr, st);
+    if (rc) return rc;
+  }
+
+  // 1) the pyramid: up to four levels per pass over the previous top level
+  for (int base = fuse_l1 ? 1 : 0; base + 1 < levels;) {
+    const int nl = std::min(GS_MAX_LEVELS, levels - 1 - base);
+    const ssk_planes& s = lv[base].planes;
+    PyramidArgs pa{};
+    pa.src_r = static_cast<const unsigned char*>(s.ref);
+    pa.src_d = static_cast<const unsigned char*>(s.dist);
+    pa.src_rp = s.row_pitch;
+    pa.src_fp = s.frame_pitch;
+    for (int i = 0; i < nl; ++i) {
+      const ssk_planes& d = lv[base + 1 + i].planes;
+      pa.dst_r[i] = const_cast<unsigned char*>(static_cast<const unsigned char*>(d.ref));
+      pa.dst_d[i] = const_cast<unsigned char*>(static_cast<const unsigned char*>(d.dist));
+      pa.dst_rp[i] = d.row_pitch;
+      pa.dst_fp[i] = d.frame_pitch;
+      pa.hl[i] = d.h;
+      pa.wl[i] = d.w;
+    }
+    rc = launch_pyramid(pa, s.dtype, lv[base + 1].planes.dtype, nl, p->n, st);
+    if (rc) return rc;
+    base += nl;
+  }
+
+  // 2) SSIM per level: level 0 alone (input type, unless already run fused), the
+  //    coarser levels batched
+  for (int l = fuse_l1 ? 1 : 0; l < levels;) {
     if (l == 0 || !plans[l].gauss || plans[l].ga.vcols != GS_THREADS) {  // wide levels launch alone
       rc = run_plan(plans[l], const_cast<double*>(fa.partials[l]), nullptr, nullptr, st);
       if (rc) return rc;

@@ -279,6 +279,51 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
     }
   };
 
+  // ---------------- fused pyramid level 1 (producers, wide u8 kernel) ----------------
+  // Each CTA owns input rows [y0, own_end) (the last segment also the K-1 tail rows)
+  // and columns [c0, c0 + TW) (the last strip up to w); at chunk c it turns the
+  // staged rows [y0 + cG, y0 + (c+1)G) -- all remaining owned rows at the last
+  // chunk -- into 2x2 block sums, exactly what pyramid_kernel writes for level 1.
+  auto level1 = [&](const int c) {
+    const bool last_seg = seg == nseg - 1, last_strip = strip == nstrips - 1;
+    const int own_end = last_seg ? a.h : y1;
+    const int rlo = y0 + c * G;
+    const int rhi = (c == nchunks - 1) ? own_end : min(rlo + G, own_end);
+    const int yb = rlo >> 1, ye = min(rhi >> 1, a.l1_h);
+    const int xb = c0 >> 1, xe = min((last_strip ? a.w : c0 + TW) >> 1, a.l1_w);
+    const int nx = xe - xb, ny = ye - yb;
+    if (nx <= 0 || ny <= 0) return;
+    // 4 level-1 samples per item: two 8-byte shared loads per image (rows 2y, 2y+1),
+    // pairwise byte sums on packed 16-bit lanes, one 8-byte store (xb is a multiple of 4)
+    const int nq = (nx + 3) >> 2;
+    for (int i = tid; i < nq * ny; i += VC) {
+      const int yy = yb + i / nq, x4 = xb + 4 * (i % nq);
+      const int col = 2 * x4 - c0;
+      const int s0 = (2 * yy - y0) % RR, s1 = (2 * yy + 1 - y0) % RR;
+      const int nvalid = min(4, xe - x4);
+#pragma unroll
+      for (int im = 0; im < 4; ++im) {
+        if ((im & 1) && !has1) continue;
+        const uint2 a0 = *reinterpret_cast<const uint2*>(raw + (s0 * 4 + im) * RB + col);
+        const uint2 a1 = *reinterpret_cast<const uint2*>(raw + (s1 * 4 + im) * RB + col);
+        // [b0 b1 b2 b3] -> 16-bit lanes (b0 + b1, b2 + b3); four rows-bytes add without carry
+        const unsigned lo = (a0.x & 0x00FF00FFu) + ((a0.x >> 8) & 0x00FF00FFu) + (a1.x & 0x00FF00FFu) +
+                            ((a1.x >> 8) & 0x00FF00FFu);
+        const unsigned hi = (a0.y & 0x00FF00FFu) + ((a0.y >> 8) & 0x00FF00FFu) + (a1.y & 0x00FF00FFu) +
+                            ((a1.y >> 8) & 0x00FF00FFu);
+        unsigned short* dst = ((im & 2) ? a.l1_dist : a.l1_ref) + (long long)((im & 1) ? f1 : f0) * a.l1_fp +
+                              (long long)yy * a.l1_rp + x4;
+        if (nvalid == 4) {
+          *reinterpret_cast<uint2*>(dst) = make_uint2(lo, hi);
+        } else {
+          const unsigned short v4[4] = {(unsigned short)(lo & 0xFFFF), (unsigned short)(lo >> 16),
+                                        (unsigned short)(hi & 0xFFFF), (unsigned short)(hi >> 16)};
+          for (int j = 0; j < nvalid; ++j) dst[j] = v4[j];
+        }
+      }
+    }
+  };
+
   // ---------------- H pass + epilogue: thread = (row, 8 columns) ----------------
   auto hpass = [&](const int c, const unsigned char* vbuf) {
     const int orow = y0 + c * G + hg;
@@ -412,6 +457,9 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
           cp_async_wait<0>();
         }
         named_sync(1, VC);                                           // chunk c's raw rows visible
+        if constexpr (VC == 256 && ES == 1) {
+          if (a.l1_ref) level1(c);
+        }
         if (c >= NB) named_sync(2 + NB + b, 2 * VC);                 // consumers released tile b
         vpass(c, vbuf0 + b * VBYTES);
         named_arrive(2 + b, 2 * VC);                                 // tile b full

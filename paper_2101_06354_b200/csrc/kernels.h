@@ -29,6 +29,12 @@ struct GaussArgs {
   double* partials;           // [n][gridDim.y][gridDim.x][3]; gridDim.z = ceil(n / 2) frame pairs
   void* maps;                 // float32 [n][planes][gh][gw]
   long long map_plane, map_frame;
+  // optional fused MS-SSIM level 1 (u16 sums of 2x2 blocks) written by the producer warps
+  // of the wide warp-specialised u8 kernel from the rows they stage anyway; null = off
+  unsigned short* l1_ref;
+  unsigned short* l1_dist;
+  long long l1_rp, l1_fp;     // elements
+  int l1_h, l1_w;
 };
 
 constexpr int GS_MAX_LEVELS = 4;  // pyramid levels fused into one multi-level launch
