@@ -253,6 +253,32 @@ def test_full_1080p_gauss_ssim_and_msssim(cuda, oracle):
     assert np.max(np.abs(maps.cs_map.values - wcs)) < MAP_TOL
 
 
+def test_fused_level1_odd_geometry_and_batch(cuda, oracle):
+    """The level-0 kernel writes pyramid level 1 (wide u8 path): odd frame sizes, several
+    strips / segments and an odd batch (a lone frame in the last packed pair)."""
+    import torch
+    from paper_2101_06354_b200 import synth
+
+    rng = np.random.default_rng(4711)
+    h, w = 517, 963  # odd: the last input row / column drop out of level 1
+    frames = []
+    for _ in range(3):
+        a = synth.inv_f_noise(rng, h, w, 255.0).astype(np.uint8)
+        b = np.clip(a.astype(int) + rng.integers(-20, 21, a.shape), 0, 255).astype(np.uint8)
+        frames.append((a, b))
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    spec = P.MultiscaleSpec.product(4)
+    ref = torch.from_numpy(np.stack([f[0] for f in frames])).to(cuda)
+    dist = torch.from_numpy(np.stack([f[1] for f in frames])).to(cuda)
+    got = P.msssim_batch(ref, dist, cfg, spec).cpu().numpy()
+    for i, (a, b) in enumerate(frames):
+        want = oracle.msssim(a, b, 4, shape="gauss", k=11, sigma=1.5)
+        assert abs(got[i] - want) < SCORE_TOL
+        lv = P.scale_scores(a, b, cfg, 4)
+        assert np.max(np.abs(np.array(lv) - np.array(oracle.scale_scores(a, b, 4, shape="gauss", k=11, sigma=1.5)))) \
+            < SCORE_TOL
+
+
 def test_full_4k_10bit_box_sums_bit_exact(cuda, oracle):
     from paper_2101_06354_b200 import synth
 
