@@ -54,15 +54,6 @@ def ssim_batch(ref, dist, config: SsimConfig = SsimConfig(), stream=None):
     return ssim_terms_batch(ref, dist, config, stream).score
 
 
-def combine_levels(level_means, spec: MultiscaleSpec):
-    """combine_scale_scores (src/multiscale.py:62-74) over a [n, L] device tensor."""
-    torch = nat.torch_mod()
-    exps = torch.tensor(spec.effective_exponents(), dtype=torch.float64, device=level_means.device)
-    if spec.aggregation == "sum":
-        return (level_means * exps).sum(dim=1)
-    return torch.pow(torch.clamp_min(level_means, 0.0), exps).prod(dim=1)
-
-
 def msssim_batch(ref, dist, config: SsimConfig = SsimConfig(), spec: Optional[MultiscaleSpec] = None,
                  with_ssim: bool = False, stream=None):
     """MS-SSIM per frame pair ([n] float64 device tensor).

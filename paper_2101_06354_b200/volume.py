@@ -124,15 +124,21 @@ class RollingVolume:
         nat.raise_for(rc, "volume refresh")
 
     def direct_sums(self) -> list:
-        """Sums recomputed from the buffered frames (drift oracle, host float64)."""
+        """Sums recomputed from scratch over the buffered frames (src/spatiotemporal.py:103-115),
+        on the device into fresh planes: the drift check against ``temporal_sums``."""
         if not self._buffer:
             raise ValidationError("no frames buffered")
-        out = [np.zeros(self._dims) for _ in range(5)]
-        for ra, rb in self._buffer:
-            a, b = ra.double().cpu().numpy(), rb.double().cpu().numpy()
-            for s, t in zip(out, (a, b, a * a, b * b, a * b)):
-                s += t
-        return out
+        torch = nat.torch_mod()
+        fresh = torch.zeros_like(self._planes)
+        h, w = self._dims
+        vol = nat.Volume(planes=fresh.data_ptr(), is_float=int(self._is_float), h=h, w=w,
+                         depth=max(1, self.depth), pitch=fresh.stride(1))
+        lib = nat.lib()
+        for i, (ra, rb) in enumerate(self._buffer):
+            rc = lib.ssk_volume_update(ctypes.byref(vol), ra.data_ptr(), rb.data_ptr(), None, None, self._code,
+                                       ra.stride(0), 0 if i == 0 else 1, nat.stream_handle())
+            nat.raise_for(rc, "volume direct sums")
+        return [p.double().cpu().numpy() for p in fresh]
 
     def temporal_sums(self) -> list:
         if self._planes is None:
