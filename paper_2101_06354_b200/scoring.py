@@ -66,7 +66,12 @@ def ssim_map(ref: PlaneLike, dist: PlaneLike, config: SsimConfig = SsimConfig())
 
 
 def mssim(maps: Union[SsimTermMaps, QualityMap, np.ndarray]) -> float:
-    """Mean of a quality map (src/ssim.py:55-65)."""
+    """Mean of a quality map (src/ssim.py:55-65), pooled on the device ('am' pooler).
+
+    The throughput path never materialises maps (``ssim_score`` pools inside the
+    SSIM kernel); this is the reference's map-level entry point."""
+    from .pooling import pool_spatial
+
     if isinstance(maps, SsimTermMaps):
         v = maps.q_map.values
     elif isinstance(maps, QualityMap):
@@ -75,7 +80,7 @@ def mssim(maps: Union[SsimTermMaps, QualityMap, np.ndarray]) -> float:
         v = np.asarray(maps, dtype=np.float64)
     if v.size == 0:
         raise EmptyMap("cannot average an empty quality map")
-    return float(v.mean())
+    return pool_spatial(v, "am")
 
 
 def ssim_terms(ref: PlaneLike, dist: PlaneLike, config: SsimConfig = SsimConfig()) -> tuple[float, float, float]:

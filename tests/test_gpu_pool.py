@@ -169,3 +169,13 @@ def test_scaled_msssim_and_non_pow2_factor(cuda, oracle):
                                                 multiscale=P.MultiscaleSpec.product(3))).score
     x, y = oracle.box_downsample(a, 4), oracle.box_downsample(b, 4)
     assert got == pytest.approx(oracle.msssim(x, y, 3, shape="rect", k=5), abs=1e-12)
+
+
+def test_mssim_pools_on_device(cuda):
+    rng = np.random.default_rng(8)
+    v = rng.uniform(-0.2, 1.0, (37, 41))
+    assert P.mssim(v) == pytest.approx(float(v.mean()), rel=1e-14)
+    maps = P.ssim_map(rng.integers(0, 256, (40, 50)).astype(np.uint8), rng.integers(0, 256, (40, 50)).astype(np.uint8))
+    assert P.mssim(maps) == pytest.approx(float(maps.q_map.values.mean()), rel=1e-14)
+    with pytest.raises(E.EmptyMap):
+        P.mssim(np.zeros((0, 3)))
