@@ -157,7 +157,10 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
   constexpr int ES = (int)sizeof(TIN);
   constexpr int RB = ((TWI * ES + 15) / 16) * 16;  // raw row bytes per image
   constexpr int NCH = RB / 16;
-  constexpr int RR = 2 * G + K - 1;                 // raw ring rows
+  // raw ring rows: the warp-specialised kernel stages chunk c+1 while chunk c is read
+  // (2G + K - 1); the classic kernel refills the G oldest rows right after its V pass,
+  // so the copy overlaps the H pass and the ring needs only the G + K - 1 rows of a chunk
+  constexpr int RR = WS ? 2 * G + K - 1 : G + K - 1;
   constexpr int NH = (K + 1) / 2;
   constexpr int NP = 8 + K - 1;                     // V values read per H item
   static_assert(TWI <= VC, "strip wider than the CTA");
@@ -431,15 +434,11 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
 
   if constexpr (!WS) {
     for (int c = 0; c < nchunks; ++c) {
-      if (c + 1 < nchunks) {
-        stage_rows(y0 + (c + 1) * G + K - 1, y0 + (c + 2) * G + K - 1);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      __syncthreads();
+      cp_async_wait<0>();
+      __syncthreads();  // chunk c's rows landed; the previous H pass is done with the V tile
       vpass(c, vbuf0);
-      __syncthreads();
+      __syncthreads();  // V tile complete; the chunk's G oldest raw rows are free
+      if (c + 1 < nchunks) stage_rows(y0 + (c + 1) * G + K - 1, y0 + (c + 2) * G + K - 1);
       hpass(c, vbuf0);
     }
   } else {
@@ -520,11 +519,12 @@ __global__ void __launch_bounds__(WS ? 2 * GS_THREADS : GS_THREADS, WS ? 2 : 4)
   gauss_body<K, TIN, NM, WS, GS_THREADS>(p.lv[lv], local % ns, local / ns, blockIdx.z, ns, p.nseg[lv]);
 }
 
-template <int K, typename TIN, int NM, int VC = GS_THREADS>
+template <int K, typename TIN, int NM, int VC = GS_THREADS, bool WS = true>
 inline size_t smem_bytes() {
   constexpr int TWI = tw_of(K, VC) + K - 1;
   constexpr int RB = ((TWI * (int)sizeof(TIN) + 15) / 16) * 16;
-  return (size_t)(2 * G + K - 1) * 4 * RB + (size_t)NM * G * vp_of(VC);
+  constexpr int RR = WS ? 2 * G + K - 1 : G + K - 1;
+  return (size_t)RR * 4 * RB + (size_t)NM * G * vp_of(VC);
 }
 
 template <int K, typename TIN, int NM, int VC>
@@ -547,7 +547,7 @@ int launch_nm(const GaussArgs& a, dim3 grid, cudaStream_t st) {
   }
   if (NM == 4 && gauss_ws_enabled()) return launch_ws<K, TIN, NM, GS_THREADS>(a, grid, st);
   auto fn = gauss_pair_kernel<K, TIN, NM>;
-  const size_t smem = smem_bytes<K, TIN, NM>();
+  const size_t smem = smem_bytes<K, TIN, NM, GS_THREADS, false>();
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SSK_E_CUDA;
   fn<<<grid, GS_THREADS, smem, st>>>(a);
@@ -567,7 +567,8 @@ int launch_levels_one(const GaussLevels& p, dim3 grid, cudaStream_t st) {
   // (small tiles, 3-4 CTAs/SM); SSK_GAUSS_WS=2 forces the warp-specialised variant
   const bool ws = gauss_ws_level() >= 2;
   auto fn = ws ? gauss_levels_kernel<K, TIN, 4, true> : gauss_levels_kernel<K, TIN, 4, false>;
-  const size_t smem = smem_bytes<K, TIN, 4>() + (ws ? (size_t)(GS_NBUF - 1) * 4 * G * vp_of(GS_THREADS) : 0);
+  const size_t smem = ws ? smem_bytes<K, TIN, 4>() + (size_t)(GS_NBUF - 1) * 4 * G * vp_of(GS_THREADS)
+                        : smem_bytes<K, TIN, 4, GS_THREADS, false>();
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SSK_E_CUDA;
   fn<<<grid, ws ? 2 * GS_THREADS : GS_THREADS, smem, st>>>(p);
