@@ -72,7 +72,16 @@ from .scoring import (
 )
 from .video import FrameScore, SequenceScorer, gather_frame_scores, score_frame_pair, score_sequence, shard_bounds
 from .ingest import FrameSource, StreamHeader, open_raw, open_y4m, score_files, write_planar_raw, write_y4m
-from .volume import REFRESH_INTERVAL, RollingVolume, msssim3d, push_frame, ssim3d_map, ssim3d_series
+from .volume import (
+    REFRESH_INTERVAL,
+    RollingVolume,
+    msssim3d,
+    push_frame,
+    shard_with_halo,
+    ssim3d_map,
+    ssim3d_series,
+    ssim3d_series_shard,
+)
 
 __version__ = "0.1.0"
 
@@ -109,4 +118,5 @@ __all__ = [
     "FrameSource", "StreamHeader", "open_raw", "open_y4m", "score_files", "write_planar_raw", "write_y4m",
     # spatio-temporal (SSIM-3D)
     "REFRESH_INTERVAL", "RollingVolume", "msssim3d", "push_frame", "ssim3d_map", "ssim3d_series",
+    "shard_with_halo", "ssim3d_series_shard",
 ]

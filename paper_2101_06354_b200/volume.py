@@ -210,6 +210,35 @@ def ssim3d_series(ref_frames: Iterable[PlaneLike], dist_frames: Iterable[PlaneLi
     return ScoreSeries(np.asarray(scores))
 
 
+def shard_with_halo(n_frames: int, rank: int, world: int, kt: int) -> tuple[int, int, int]:
+    """(first frame to push, first frame to score, stop) of ``rank``'s contiguous block:
+    SSIM-3D shards need the Kt-1 frames before their block as a halo."""
+    from .video import shard_bounds
+
+    if not isinstance(kt, int) or kt < 1:
+        raise ValidationError(f"temporal window must be an integer >= 1, got {kt!r}")
+    start, stop = shard_bounds(n_frames, rank, world)
+    return max(0, start - (kt - 1)), start, stop
+
+
+def ssim3d_series_shard(ref_frames, dist_frames, kt: int, rank: int, world: int,
+                        config: SsimConfig = SsimConfig()) -> ScoreSeries:
+    """This rank's slice of ``ssim3d_series``: the halo frames are pushed unscored, then
+    the rank's own frames are scored.  Concatenating every rank's slice in rank order
+    gives the unsharded series (bit-exactly for integer frames, whose rolling sums are
+    exact; float volumes refresh on their own push count)."""
+    if len(ref_frames) != len(dist_frames):
+        raise DimensionMismatch("reference and distorted streams differ in length")
+    lo, start, stop = shard_with_halo(len(ref_frames), rank, world, kt)
+    vol = RollingVolume(kt)
+    scores = []
+    for i in range(lo, stop):
+        vol.push(ref_frames[i], dist_frames[i])
+        if i >= start:
+            scores.append(vol.terms(config.window, config)[0])
+    return ScoreSeries(np.asarray(scores))
+
+
 def msssim3d(ref_frames: Iterable[PlaneLike], dist_frames: Iterable[PlaneLike], kt: int,
              spec: Optional[MultiscaleSpec] = None, config: SsimConfig = SsimConfig()) -> ScoreSeries:
     """Multiscale 3-D SSIM, one rolling volume per scale (src/spatiotemporal.py:174-207)."""

@@ -461,6 +461,16 @@ def test_ssim3d_against_golden(cuda, golden):
     assert np.max(np.abs(got - golden["vol/ms3d"])) < 1e-12
 
 
+def test_ssim3d_sharded_with_halo_equals_unsharded(cuda, golden):
+    fa = [golden[f"vol/ref{i}"] for i in range(7)]
+    fb = [golden[f"vol/dist{i}"] for i in range(7)]
+    cfg = P.SsimConfig(window=P.WindowSpec.rectangular(7))
+    full = P.ssim3d_series(fa, fb, 3, cfg).scores
+    for world in (2, 3):
+        parts = [P.ssim3d_series_shard(fa, fb, 3, r, world, cfg).scores for r in range(world)]
+        assert np.array_equal(np.concatenate(parts), full)
+
+
 def test_ssim3d_float_refresh_against_golden(cuda, golden):
     fa = [golden[f"vol/ref{i}"].astype(np.float64) / 3.0 for i in range(7)]
     fb = [golden[f"vol/dist{i}"].astype(np.float64) / 3.0 for i in range(7)]

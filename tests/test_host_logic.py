@@ -202,3 +202,12 @@ def test_media_ingest_y4m_and_raw(tmp_path):
     bad.write_bytes(b"YUV4MPEG2 W8 H6\nFRAME\n" + b"\0" * 10)
     with pytest.raises(E.TruncatedFrame):
         ingest.open_y4m(bad)
+
+
+def test_ssim3d_shard_halo_bounds():
+    # contiguous blocks, each preceded by the kt-1 frames its first window needs
+    got = [P.shard_with_halo(10, r, 3, 3) for r in range(3)]
+    assert got == [(0, 0, 4), (2, 4, 7), (5, 7, 10)]
+    assert [P.shard_with_halo(10, r, 3, 1) for r in range(3)] == [(0, 0, 4), (4, 4, 7), (7, 7, 10)]
+    with pytest.raises(E.ValidationError):
+        P.shard_with_halo(10, 0, 2, 0)
