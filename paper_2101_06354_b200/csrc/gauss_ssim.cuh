@@ -240,12 +240,15 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
       for (int m = 0; m < NM; ++m)
 #pragma unroll
         for (int r = 0; r < G; ++r) acc[m][r] = 0ull;
+      // ring rows s0, s0+1, ... : one base before the wrap point, one after, so each row's
+      // address is a select plus an immediate offset
       const int s0 = (c * G) % RR;
+      const int wrap = RR - s0;
+      const unsigned char* pa = raw + s0 * 4 * RB + tid * ES;
+      const unsigned char* pb = pa - RR * 4 * RB;
 #pragma unroll
       for (int u = 0; u < G + K - 1; ++u) {
-        int slot = s0 + u;
-        slot = slot >= RR ? slot - RR : slot;
-        const unsigned char* rp = raw + slot * 4 * RB + tid * ES;
+        const unsigned char* rp = (u < wrap ? pa : pb) + u * 4 * RB;
         const u64 X = fma2(pk(raw_to_float<TIN>(rp), raw_to_float<TIN>(rp + RB)), scale2, bias2);
         const u64 Y = fma2(pk(raw_to_float<TIN>(rp + 2 * RB), raw_to_float<TIN>(rp + 3 * RB)), scale2, bias2);
         u64 P[NM];
