@@ -300,12 +300,16 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
     const int nx = xe - xb, ny = ye - yb;
     if (nx <= 0 || ny <= 0) return;
     // 4 level-1 samples per item: two 8-byte shared loads per image (rows 2y, 2y+1),
-    // pairwise byte sums on packed 16-bit lanes, one 8-byte store (xb is a multiple of 4)
+    // pairwise byte sums on packed 16-bit lanes, one 8-byte store (xb is a multiple of 4).
+    // Item (row, quad) = (tid / 32 + k * VC / 32, tid % 32): at most 32 quads per row
+    // (nx <= (TW + K - 1) / 2), so no division; RR is even, so row 2y+1 sits in slot s0 + 1.
+    static_assert(RR % 2 == 0 && (TW + K - 1) / 2 <= 128, "level-1 item mapping");
     const int nq = (nx + 3) >> 2;
-    for (int i = tid; i < nq * ny; i += VC) {
-      const int yy = yb + i / nq, x4 = xb + 4 * (i % nq);
+    const int q = tid & 31;
+    for (int r = tid >> 5; r < ny && q < nq; r += VC >> 5) {
+      const int yy = yb + r, x4 = xb + 4 * q;
       const int col = 2 * x4 - c0;
-      const int s0 = (2 * yy - y0) % RR, s1 = (2 * yy + 1 - y0) % RR;
+      const int s0 = (2 * yy - y0) % RR, s1 = s0 + 1;
       const int nvalid = min(4, xe - x4);
 #pragma unroll
       for (int im = 0; im < 4; ++im) {
