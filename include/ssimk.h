@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SSK_ABI_VERSION 6
+#define SSK_ABI_VERSION 7
 
 /* sample storage types */
 enum {
@@ -55,7 +55,9 @@ enum {
   SSK_WANT_L = 2,      /* per-frame sum of l                                  */
   SSK_WANT_CS = 4,     /* per-frame sum of cs                                 */
   SSK_MAP_TERMS = 8,   /* write the l, cs, q maps (3 planes per frame)        */
-  SSK_MAP_STATS = 16   /* write mu1, mu2, var1, var2, cov (5 planes per frame) */
+  SSK_MAP_STATS = 16,  /* write mu1, mu2, var1, var2, cov (5 planes per frame) */
+  SSK_WANT_Q2 = 32     /* rect windows: also the per-frame sum of q^2, d_sums is then
+                          [n][4] (CoV / MD(2) pooling without a map, src/pooling.py:157-166) */
 };
 
 /* error codes */
@@ -257,6 +259,12 @@ typedef struct ssk_pooler {
 } ssk_pooler;
 
 size_t ssk_pool_workspace_bytes(const ssk_maps* m, const ssk_pooler* pool);
+/* CoV / MD(p = 2, o) pooling without a map, from the [n][4] per-frame sums of an
+ * ssk_ssim(..., SSK_WANT_Q2) pass over `count` windows (one-pass variance,
+ * ~1e-11 relative to numpy's two-pass std); d_out [n]; d_means [n][3]
+ * (nullable) = mean q, mean l, mean cs. */
+int ssk_pool_moments(const double* d_sums, int n, double count, const ssk_pooler* pool, double* d_out,
+                     double* d_means, void* stream);
 /* d_out [n] pooled scores; d_mean [n] (nullable) the plain mean of each map. */
 int ssk_pool_spatial(const ssk_maps* m, const ssk_pooler* pool, double* d_out, double* d_mean,
                      void* d_workspace, size_t workspace_bytes, void* stream);

@@ -29,10 +29,10 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libssimk.so"
 # enums (include/ssimk.h)
 U8, U16, U32, F32, F64 = 1, 2, 3, 4, 5
 RECT, GAUSS = 1, 2
-WANT_Q, WANT_L, WANT_CS, MAP_TERMS, MAP_STATS = 1, 2, 4, 8, 16
+WANT_Q, WANT_L, WANT_CS, MAP_TERMS, MAP_STATS, WANT_Q2 = 1, 2, 4, 8, 16, 32
 E_ARG, E_WINDOW, E_SHAPE, E_WORKSPACE, E_ALIGN, E_CUDA, E_LEVELS, E_TOO_SMALL = range(-1, -9, -1)
 
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 EXPORTED_SYMBOLS = (
     "ssk_abi_version",
@@ -51,6 +51,7 @@ EXPORTED_SYMBOLS = (
     "ssk_box_downsample",
     "ssk_pool_workspace_bytes",
     "ssk_pool_spatial",
+    "ssk_pool_moments",
     "ssk_color_convert",
     "ssk_qssim_workspace_bytes",
     "ssk_qssim",
@@ -198,6 +199,8 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         lib.ssk_pool_workspace_bytes.argtypes = [pM, pQ]
         lib.ssk_pool_spatial.restype = i32
         lib.ssk_pool_spatial.argtypes = [pM, pQ, vp, vp, vp, sz, vp]
+        lib.ssk_pool_moments.restype = i32
+        lib.ssk_pool_moments.argtypes = [vp, i32, ctypes.c_double, pQ, vp, vp, vp]
         pC, pD = ctypes.POINTER(Color), ctypes.POINTER(ctypes.c_double)
         lib.ssk_color_convert.restype = i32
         lib.ssk_color_convert.argtypes = [pC, i32, vp, i64, i64, vp]

@@ -65,8 +65,9 @@ __device__ __forceinline__ void emit_window(const BoxArgs& a, int frame, int ar,
 
 __device__ __forceinline__ void emit_fast(const BoxArgs& a, const uint32_t (&s)[5], double& sq, double& sl,
                                           double& scs) {
-  box_fast_terms(a, (unsigned long long)s[0], (unsigned long long)s[1], (unsigned long long)s[2],
-                 (unsigned long long)s[3], (unsigned long long)s[4], sq, sl, scs);
+  double unused = 0.0;  // q^2 sums are a running-sum-kernel feature (plan_ssim routes SSK_WANT_Q2 there)
+  box_fast_terms<BoxArgs, false>(a, (unsigned long long)s[0], (unsigned long long)s[1], (unsigned long long)s[2],
+                                 (unsigned long long)s[3], (unsigned long long)s[4], sq, sl, scs, unused);
 }
 
 // 8 samples of one row as 4 packed u16 pairs (a0|a1<<16, ...), zero past the row end

@@ -53,9 +53,11 @@ __device__ __forceinline__ BoxTerms box_terms(double s1, double s2, double q1, d
   return t;
 }
 
+template <bool Q2>
 __device__ __forceinline__ void box_emit(const BoxTerms& t, const BoxArgs& a, int frame, int ar,
-                                         int ac, double& sq, double& sl, double& scs) {
+                                         int ac, double& sq, double& sl, double& scs, double& sq2) {
   sq += t.q;
+  if constexpr (Q2) sq2 += __dmul_rn(t.q, t.q);
   sl += t.l;
   scs += t.cs;
   if (a.want & (SSK_MAP_TERMS | SSK_MAP_STATS)) {
@@ -88,7 +90,7 @@ __device__ __forceinline__ T load_sample(const unsigned char* p) {
 // MOM = true: the five per-pixel moments come precomputed from int64 planes
 // (the rolling temporal sums of a RollingVolume, src/spatiotemporal.py:60-138)
 // instead of being formed from staged x / y samples; everything else is shared.
-template <typename TIN, typename ACC, bool MOM = false, bool FAST = false>
+template <typename TIN, typename ACC, bool MOM = false, bool FAST = false, bool Q2 = false>
 __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_constant__ BoxArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double s_red[(BX_THREADS / 32) * 3];
@@ -145,7 +147,7 @@ __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_consta
   int emit_at = k, emit_slot = 0;       // next window close: after row u where u+1 == emit_at
   int bnext = 0;                        // next anchor row (relative) to close
 
-  double sq = 0.0, sl = 0.0, scs = 0.0;
+  double sq = 0.0, sl = 0.0, scs = 0.0, sq2 = 0.0;
   issue_stage(0, 0);
 
   for (int c = 0; c < nchunks; ++c) {
@@ -224,8 +226,9 @@ __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_consta
         for (int m = 0; m < 5; ++m) ws[m * a.map_plane] = (long long)sums[m];
       }
       if constexpr (FAST) {
-        box_fast_terms(a, (unsigned long long)sums[0], (unsigned long long)sums[1], (unsigned long long)sums[2],
-                       (unsigned long long)sums[3], (unsigned long long)sums[4], sq, sl, scs);
+        box_fast_terms<BoxArgs, Q2>(a, (unsigned long long)sums[0], (unsigned long long)sums[1],
+                                    (unsigned long long)sums[2],
+                       (unsigned long long)sums[3], (unsigned long long)sums[4], sq, sl, scs, sq2);
         continue;
       }
       const BoxTerms t = box_terms(__dmul_rn((double)sums[0], a.sscale1),
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_consta
                                    __dmul_rn((double)sums[2], a.sscale2),
                                    __dmul_rn((double)sums[3], a.sscale2),
                                    __dmul_rn((double)sums[4], a.sscale2), a);
-      box_emit(t, a, frame, ar, ac, sq, sl, scs);
+      box_emit<Q2>(t, a, frame, ar, ac, sq, sl, scs, sq2);
     }
     // the barrier at the top of the next chunk protects vrow
   }
@@ -241,6 +244,10 @@ __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_consta
   double v[3] = {sq, sl, scs};
   const long long part = ((long long)frame * gridDim.y + seg) * gridDim.x + strip;
   block_sum_store<3, BX_THREADS / 32>(v, s_red, a.partials + part * 3);
+  if constexpr (Q2) {
+    __shared__ double s_red2[BX_THREADS / 32];
+    store_q2<BoxArgs, BX_THREADS / 32>(a, sq2, s_red2, part);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -255,7 +262,7 @@ __global__ void __launch_bounds__(128) box_direct_kernel(const __grid_constant__
   const int ac = blockIdx.x * blockDim.x + threadIdx.x;
   const int ar = blockIdx.y * blockDim.y + threadIdx.y;
   const int frame = blockIdx.z;
-  double sq = 0.0, sl = 0.0, scs = 0.0;
+  double sq = 0.0, sl = 0.0, scs = 0.0, sq2 = 0.0;
   if (ac < a.gw && ar < a.gh) {
     const unsigned char* bx = a.ref + (long long)frame * a.frame_pitch_b;
     const unsigned char* by = a.dist + (long long)frame * a.frame_pitch_b;
@@ -285,11 +292,13 @@ __global__ void __launch_bounds__(128) box_direct_kernel(const __grid_constant__
     const BoxTerms t = box_terms(__dmul_rn((double)s1, a.sscale1), __dmul_rn((double)s2, a.sscale1),
                                  __dmul_rn((double)q1, a.sscale2), __dmul_rn((double)q2, a.sscale2),
                                  __dmul_rn((double)p, a.sscale2), a);
-    box_emit(t, a, frame, ar, ac, sq, sl, scs);
+    box_emit<true>(t, a, frame, ar, ac, sq, sl, scs, sq2);
   }
   double v[3] = {sq, sl, scs};
   const long long part = ((long long)frame * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   block_sum_store<3, 4>(v, s_red, a.partials + part * 3);
+  __shared__ double s_red2[4];
+  store_q2<BoxArgs, 4>(a, sq2, s_red2, part);
 }
 
 // ---------------------------------------------------------------------------
@@ -304,7 +313,9 @@ size_t box_smem_bytes(const BoxArgs& a, bool wide) {
 template <typename TIN, typename ACC>
 static int launch_int_t(const BoxArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   const bool fast = !(a.want & (SSK_MAP_TERMS | SSK_MAP_STATS)) && !a.wsums && a.fast_ok;
-  auto fn = fast ? box_int_kernel<TIN, ACC, false, true> : box_int_kernel<TIN, ACC, false, false>;
+  const bool q2 = a.partials2 != nullptr;
+  auto fn = fast ? (q2 ? box_int_kernel<TIN, ACC, false, true, true> : box_int_kernel<TIN, ACC, false, true, false>)
+                 : (q2 ? box_int_kernel<TIN, ACC, false, false, true> : box_int_kernel<TIN, ACC, false, false, false>);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SSK_E_CUDA;
   fn<<<grid, BX_THREADS, smem, st>>>(a);

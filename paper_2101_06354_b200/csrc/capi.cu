@@ -183,8 +183,9 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
   a.map_frame = a.map_plane * ((want & SSK_MAP_STATS) ? 5 : 3);
   a.wsums = nullptr;
   const bool integer = p->dtype == SSK_U8 || p->dtype == SSK_U16 || p->dtype == SSK_U32;
-  if (integer && box_block_supported(p->dtype, k, s, (double)k * k * stored_max * stored_max >= 4294967296.0,
-                                     stored_max)) {
+  // (q^2 sums are produced by the running-sum kernel only)
+  if (integer && !(want & SSK_WANT_Q2) &&
+      box_block_supported(p->dtype, k, s, (double)k * k * stored_max * stored_max >= 4294967296.0, stored_max)) {
     // stride divides the window: block-sum kernel (warps of 248 new columns, ~16 anchor rows per
     // segment: enough independent warps to keep HBM busy even for a handful of frames)
     pl.box_block = true;
@@ -325,7 +326,7 @@ const char* ssk_strerror(int code) {
 size_t ssk_ssim_workspace_bytes(const ssk_planes* p, const ssk_window* win) {
   Plan pl;
   if (plan_ssim(p, win, SSK_WANT_Q | SSK_WANT_L | SSK_WANT_CS, pl)) return 0;
-  return partial_bytes(pl, p->n);
+  return partial_bytes(pl, p->n) * (pl.gauss ? 1 : 2);  // rect: room for the q^2 partials
 }
 
 int ssk_ssim(const ssk_planes* p, const ssk_window* win, int want, double* d_sums, void* d_maps,
@@ -335,13 +336,20 @@ int ssk_ssim(const ssk_planes* p, const ssk_window* win, int want, double* d_sum
   if (rc) return rc;
   if (!d_sums) return SSK_E_ARG;
   if ((want & (SSK_MAP_TERMS | SSK_MAP_STATS)) && !d_maps) return SSK_E_ARG;
-  const size_t need = partial_bytes(pl, p->n);
-  if (!d_workspace || workspace_bytes < need) return SSK_E_WORKSPACE;
+  const bool q2 = (want & SSK_WANT_Q2) != 0;
+  if (q2 && pl.gauss) return SSK_E_SHAPE;
+  const size_t one = partial_bytes(pl, p->n);
+  if (!d_workspace || workspace_bytes < one * (q2 ? 2 : 1)) return SSK_E_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   double* partials = static_cast<double*>(d_workspace);
+  double* partials2 = q2 ? reinterpret_cast<double*>(static_cast<char*>(d_workspace) + one) : nullptr;
+  pl.ba.partials2 = partials2;
   int e = run_plan(pl, partials, d_maps, nullptr, st);
   if (e) return e;
-  return launch_reduce_partials(partials, (int)pl.nparts_per_frame, p->n, 3, 1.0, d_sums, 3, 0, 0, st);
+  const int cols = q2 ? 4 : 3;
+  e = launch_reduce_partials(partials, (int)pl.nparts_per_frame, p->n, 3, 1.0, d_sums, cols, 0, 0, st);
+  if (e || !q2) return e;
+  return launch_reduce_partials(partials2, (int)pl.nparts_per_frame, p->n, 1, 1.0, d_sums, 4, 3, 0, st);
 }
 
 int ssk_box_window_sums(const ssk_planes* p, int k, int stride, int64_t* d_out, void* d_workspace,

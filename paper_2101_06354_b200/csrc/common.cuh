@@ -83,19 +83,30 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // C' = C k^4 4^scale, each with one rounded add and a Newton reciprocal:
 // scores agree with the reference's float64 expression to ~1e-15.  Maps keep
 // the reference's own operation order (bit-identical) and never come here.
-template <typename Args>
+template <typename Args, bool Q2>
 __device__ __forceinline__ void box_fast_terms(const Args& a, unsigned long long s1, unsigned long long s2,
                                                unsigned long long q1, unsigned long long q2, unsigned long long p,
-                                               double& sq, double& sl, double& scs) {
+                                               double& sq, double& sl, double& scs, double& sq2) {
   const unsigned long long A = (unsigned long long)a.area_i;
   const unsigned long long p11 = s1 * s1, p22 = s2 * s2, p12 = s1 * s2;
   const unsigned long long v12 = (A * q1 - p11) + (A * q2 - p22);
   const long long cv2 = 2 * ((long long)(A * p) - (long long)p12);
   const double l = __dmul_rn(__dadd_rn((double)(2 * p12), a.c1d), rcp_nr(__dadd_rn((double)(p11 + p22), a.c1d)));
   const double cs = __dmul_rn(__dadd_rn((double)cv2, a.c2d), rcp_nr(__dadd_rn((double)v12, a.c2d)));
-  sq += __dmul_rn(l, cs);
+  const double q = __dmul_rn(l, cs);
+  sq += q;
   sl += l;
   scs += cs;
+  if constexpr (Q2) sq2 += __dmul_rn(q, q);
+}
+
+// Per-CTA sum of q^2 for SSK_WANT_Q2 (CoV / MD(2) pooling fused into the rect kernels);
+// uniform branch, so the block barrier inside is safe.
+template <typename Args, int NWARPS>
+__device__ __forceinline__ void store_q2(const Args& a, double sq2, double* scratch /*NWARPS*/, long long part) {
+  if (!a.partials2) return;
+  double v[1] = {sq2};
+  block_sum_store<1, NWARPS>(v, scratch, a.partials2 + part * 3);
 }
 
 // Number of kernels launched by this library (bench.py's gpu_launches claim).

@@ -83,6 +83,7 @@ struct BoxArgs {
   double c1, c2;
   int want;
   double* partials;           // [n][gridDim.y][gridDim.x][3]
+  double* partials2;          // optional, same layout, slot 0 = sum of q^2 (SSK_WANT_Q2)
   double* maps;               // float64 [n][planes][gh][gw]
   long long map_plane, map_frame;
   long long* wsums;           // optional int64 [n][5][gh][gw]

@@ -602,6 +602,32 @@ int launch_box_downsample_t(const ssk_planes* p, int f, void* dr, void* dd, int 
   return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
 }
 
+// ---------------------------------------------------------------------------
+// moment pooling: CoV / MD(p = 2) from the [n][4] sums of an SSK_WANT_Q2 pass
+// (sum q, sum l, sum cs, sum q^2), one thread per frame
+// ---------------------------------------------------------------------------
+__global__ void pool_moments_kernel(const double* __restrict__ sums, int n, double count, int kind, double o,
+                                    double* __restrict__ out, double* __restrict__ means) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n) return;
+  const double* s = sums + (long long)f * 4;
+  const double mq = __ddiv_rn(s[0], count);
+  const double var = fmax(__dsub_rn(__ddiv_rn(s[3], count), __dmul_rn(mq, mq)), 0.0);
+  const double sd = __dsqrt_rn(var);
+  double r;
+  if (kind == SSK_POOL_COV) {
+    r = mq == 0.0 ? NAN : __ddiv_rn(sd, mq);
+  } else {
+    r = o == 1.0 ? sd : pow(sd, o);
+  }
+  out[f] = r;
+  if (means) {
+    means[(long long)f * 3] = mq;
+    means[(long long)f * 3 + 1] = __ddiv_rn(s[1], count);
+    means[(long long)f * 3 + 2] = __ddiv_rn(s[2], count);
+  }
+}
+
 // ---- pooling plan ----
 struct PoolPlan {
   PoolArgs a{};
@@ -765,6 +791,17 @@ int ssk_box_downsample(const ssk_planes* src, int factor, void* d_dst_ref, void*
     default:
       return SSK_E_ARG;
   }
+}
+
+int ssk_pool_moments(const double* d_sums, int n, double count, const ssk_pooler* pool, double* d_out,
+                     double* d_means, void* stream) {
+  if (!d_sums || !d_out || !pool || n < 1 || !(count > 0)) return SSK_E_ARG;
+  const bool md2 = pool->kind == SSK_POOL_MD && pool->p == 2.0 && pool->o > 0;
+  if (pool->kind != SSK_POOL_COV && !md2) return SSK_E_ARG;
+  pool_moments_kernel<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(d_sums, n, count, pool->kind,
+                                                                                     pool->o, d_out, d_means);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
 }
 
 size_t ssk_pool_workspace_bytes(const ssk_maps* m, const ssk_pooler* pool) {

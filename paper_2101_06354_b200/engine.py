@@ -147,7 +147,8 @@ def grid_shape(h: int, w: int, k: int, s: int) -> tuple[int, int]:
 def ssim(pair: DevicePair, window, c1: float, c2: float, want: int, stream=None):
     """Fused SSIM over a device batch.
 
-    Returns (sums [n,3] float64 device tensor (sum q, sum l, sum cs), maps or None).
+    Returns (sums [n,3] float64 device tensor (sum q, sum l, sum cs; a 4th column sum q^2
+    with SSK_WANT_Q2), maps or None).
     Maps: SSK_MAP_TERMS -> [n,3,gh,gw] (l, cs, q); SSK_MAP_STATS -> [n,5,gh,gw];
     float32 for Gaussian windows, float64 for rect windows.
     """
@@ -157,7 +158,7 @@ def ssim(pair: DevicePair, window, c1: float, c2: float, want: int, stream=None)
     planes = pair.planes()
     win = nat.make_window(window, c1, c2)
     dev = pair.ref.device
-    sums = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    sums = torch.empty((n, 4 if want & nat.WANT_Q2 else 3), dtype=torch.float64, device=dev)
     maps = None
     if want & (nat.MAP_TERMS | nat.MAP_STATS):
         gh, gw = grid_shape(h, w, window.k, window.stride)

@@ -137,6 +137,25 @@ def luma_records(pair: engine.DevicePair, config: SsimConfig, factor: Optional[i
         sums, _ = engine.ssim(pair, win, config.c1, config.c2, want, stream)
         means = engine.frame_means(sums, gh * gw)
         return FrameRecords(means[:, 0], means[:, 0], means[:, 1], means[:, 2])
+    if win.shape == "rect" and (pool.kind == "cov" or (pool.kind == "md" and pool.p == 2.0)):
+        # dispersion of the map from sum q and sum q^2 accumulated inside the rect kernel
+        # (exact integer moments there; no map is written, no pooling pass): the
+        # one-pass variance differs from numpy's two-pass std by ~1e-11 relative
+        import ctypes
+
+        torch = nat.torch_mod()
+        sums, _ = engine.ssim(pair, win, config.c1, config.c2, want | nat.WANT_Q2, stream)
+        pooled = torch.empty((n,), dtype=torch.float64, device=sums.device)
+        means = torch.empty((n, 3), dtype=torch.float64, device=sums.device)
+        native = pool.native()
+        rc = nat.lib().ssk_pool_moments(sums.data_ptr(), n, float(gh * gw), ctypes.byref(native), pooled.data_ptr(),
+                                        means.data_ptr(), nat.stream_handle(stream))
+        nat.raise_for(rc, "moment pooling")
+        if strict and pool.kind == "cov" and bool(torch.isnan(pooled).any()):
+            from .errors import ZeroMeanCoV
+
+            raise ZeroMeanCoV("coefficient of variation is undefined for a zero-mean input")
+        return FrameRecords(pooled, means[:, 0], means[:, 1], means[:, 2])
     sums, maps = engine.ssim(pair, win, config.c1, config.c2, want | nat.MAP_TERMS, stream)
     mu1 = None
     if pool.kind == "lw":

@@ -179,3 +179,17 @@ def test_mssim_pools_on_device(cuda):
     assert P.mssim(maps) == pytest.approx(float(maps.q_map.values.mean()), rel=1e-14)
     with pytest.raises(E.EmptyMap):
         P.mssim(np.zeros((0, 3)))
+
+
+def test_fused_moment_pooling_matches_map_pooling(cuda):
+    """CoV / MD(2) from the in-kernel sum of q^2 (no map) equals pooling the returned map."""
+    rng = np.random.default_rng(12)
+    a = rng.integers(0, 256, (96, 130)).astype(np.uint8)
+    b = np.clip(a.astype(int) + rng.integers(-30, 31, a.shape), 0, 255).astype(np.uint8)
+    for win in (P.WindowSpec.rectangular(11, stride=5), P.WindowSpec.rectangular(8), P.WindowSpec.rectangular(7, stride=2)):
+        for sel in ("cov", "md:p=2,o=1", "md:p=2,o=3"):
+            cfg = P.SsimConfig(window=win, spatial_pool=sel)
+            fused = P.score_frame_pair(a, b, cfg)
+            q = P.ssim_map(a, b, P.SsimConfig(window=win)).q_map
+            assert fused.score == pytest.approx(P.pool_spatial(q, sel), rel=1e-10, abs=1e-14), (win, sel)
+            assert fused.am == pytest.approx(float(q.values.mean()), abs=1e-14)
