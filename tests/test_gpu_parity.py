@@ -279,6 +279,21 @@ def test_fused_level1_odd_geometry_and_batch(cuda, oracle):
             < SCORE_TOL
 
 
+@pytest.mark.parametrize("k,sigma,levels,h,w", [(7, 1.0, 2, 301, 650), (15, 2.3, 3, 422, 703), (17, 2.7, 3, 480, 996)])
+def test_fused_level1_window_sizes(cuda, oracle, k, sigma, levels, h, w):
+    """Wide-strip kernel + fused level 1 across window sizes (k <= 17 takes the wide path)."""
+    from paper_2101_06354_b200 import synth
+
+    rng = np.random.default_rng(k * 100 + levels)
+    a = synth.inv_f_noise(rng, h, w, 255.0).astype(np.uint8)
+    b = np.clip(a.astype(int) + rng.integers(-25, 26, a.shape), 0, 255).astype(np.uint8)
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(sigma, k=k))
+    win = dict(shape="gauss", k=k, sigma=sigma)
+    got = P.scale_scores(a, b, cfg, levels)
+    want = oracle.scale_scores(a, b, levels, **win)
+    assert np.max(np.abs(np.array(got) - np.array(want))) < SCORE_TOL
+
+
 def test_full_4k_10bit_box_sums_bit_exact(cuda, oracle):
     from paper_2101_06354_b200 import synth
 
