@@ -23,7 +23,7 @@ from . import _native as nat
 from . import engine
 from .errors import EngineShapeMismatch, NonPositiveSigma, ValidationError, WindowLargerThanImage, WindowOutOfBounds
 from .options import WindowSpec, default_gaussian_size
-from .planes import LumaPlane, PlaneLike, plane_bit_depth, plane_data, validate_frame_pair
+from .planes import PlaneLike, plane_bit_depth, plane_data, validate_frame_pair
 
 TABLE_IDS = ("sum1", "sum2", "sq1", "sq2", "prod")
 

@@ -16,6 +16,7 @@ runs as a handful of launches per batch with only scalars leaving the GPU.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -141,8 +142,6 @@ def luma_records(pair: engine.DevicePair, config: SsimConfig, factor: Optional[i
         # dispersion of the map from sum q and sum q^2 accumulated inside the rect kernel
         # (exact integer moments there; no map is written, no pooling pass): the
         # one-pass variance differs from numpy's two-pass std by ~1e-11 relative
-        import ctypes
-
         torch = nat.torch_mod()
         sums, _ = engine.ssim(pair, win, config.c1, config.c2, want | nat.WANT_Q2, stream)
         pooled = torch.empty((n,), dtype=torch.float64, device=sums.device)

@@ -14,7 +14,6 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import _native as nat
 from . import engine
 from .errors import TooManyLevels, TooSmall, ValidationError
 from .moments import check_fit, resolve_engine
