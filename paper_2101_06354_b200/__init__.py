@@ -58,7 +58,16 @@ from .adaptation import (
     sast_factor,
     viewing_geometry,
 )
-from .pipeline import FrameRecords, PipelineSpec, expand_preset, luma_records, preset_specs, score_batch
+from .pipeline import (
+    FRAME_FIELDS,
+    FrameRecords,
+    PipelineSpec,
+    expand_preset,
+    luma_records,
+    preset_specs,
+    run_score,
+    score_batch,
+)
 from .pyramid import combine_scale_scores, dyadic_downsample, msssim, scale_scores
 from .scoring import (
     SsimTermMaps,
@@ -71,7 +80,22 @@ from .scoring import (
     weber_luminance_term,
 )
 from .video import FrameScore, SequenceScorer, gather_frame_scores, score_frame_pair, score_sequence, shard_bounds
-from .ingest import FrameSource, StreamHeader, open_raw, open_y4m, score_files, write_planar_raw, write_y4m
+from .ingest import (
+    FrameSource,
+    StreamHeader,
+    VideoStream,
+    format_float,
+    open_raw,
+    open_stream,
+    open_y4m,
+    read_planar_raw,
+    read_pnm,
+    read_y4m,
+    score_files,
+    write_planar_raw,
+    write_report,
+    write_y4m,
+)
 from .volume import (
     REFRESH_INTERVAL,
     RollingVolume,
@@ -110,12 +134,14 @@ __all__ = [
     "box_downsample", "enhanced_scale_factor", "legacy_scale_factor", "policy_factor", "round_half_away",
     "sast_factor", "viewing_geometry",
     # pipeline contract / presets
-    "FrameRecords", "PipelineSpec", "expand_preset", "luma_records", "preset_specs", "score_batch",
+    "FRAME_FIELDS", "FrameRecords", "PipelineSpec", "expand_preset", "luma_records", "preset_specs", "run_score",
+    "score_batch",
     # batched device API / sequences / multi-GPU
     "FrameTerms", "HostBatchScorer", "color_batch", "msssim_batch", "ssim_batch", "ssim_terms_batch",
     "SequenceScorer", "gather_frame_scores", "score_sequence", "shard_bounds", "FrameScore", "score_frame_pair",
     # media ingest
-    "FrameSource", "StreamHeader", "open_raw", "open_y4m", "score_files", "write_planar_raw", "write_y4m",
+    "FrameSource", "StreamHeader", "VideoStream", "format_float", "open_raw", "open_stream", "open_y4m",
+    "read_planar_raw", "read_pnm", "read_y4m", "score_files", "write_planar_raw", "write_report", "write_y4m",
     # spatio-temporal (SSIM-3D)
     "REFRESH_INTERVAL", "RollingVolume", "msssim3d", "push_frame", "ssim3d_map", "ssim3d_series",
     "shard_with_halo", "ssim3d_series_shard",

@@ -108,3 +108,11 @@ class TruncatedFrame(SsimkitError):
 
 class SizeNotMultiple(SsimkitError):
     """Raw file size is not a whole multiple of the frame size."""
+
+
+class UnsupportedMaxval(SsimkitError):
+    """PNM maxval is zero or exceeds the 16-bit range."""
+
+
+class LengthMismatch(SsimkitError):
+    """Paired sequences differ in length."""

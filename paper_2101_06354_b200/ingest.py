@@ -16,8 +16,16 @@ from typing import Iterator, Optional, Sequence
 
 import numpy as np
 
-from .errors import BadHeader, BadMagic, SizeNotMultiple, TruncatedFrame, UnsupportedChroma, ValidationError
-from .planes import CHROMA_420, CHROMA_444
+from .errors import (
+    BadHeader,
+    BadMagic,
+    SizeNotMultiple,
+    TruncatedFrame,
+    UnsupportedChroma,
+    UnsupportedMaxval,
+    ValidationError,
+)
+from .planes import CHROMA_420, CHROMA_444, SPACE_RGB, SPACE_YCBCR, ColorFrame, LumaPlane
 
 Y4M_MAGIC = b"YUV4MPEG2"
 _Y4M_CHROMA = {"420": CHROMA_420, "420jpeg": CHROMA_420, "420mpeg2": CHROMA_420, "444": CHROMA_444, "mono": "mono"}
@@ -161,14 +169,28 @@ def open_raw(path, width: int, height: int, bit_depth: int = 8, chroma: str = CH
     return FrameSource(path, header, [i * fbytes for i in range(size // fbytes)])
 
 
-def write_y4m(path, frames, width: int, height: int, chroma: str = CHROMA_420, frame_rate=(30, 1)) -> None:
-    """Write 8-bit frames (tuples of planes, or luma planes for mono) as YUV4MPEG2."""
+def _frame_planes(fr) -> tuple:
+    """Planes of a frame given as LumaPlane / ColorFrame (reference types) or arrays."""
+    if isinstance(fr, LumaPlane):
+        return (fr.samples,)
+    if isinstance(fr, ColorFrame):
+        return tuple(fr.channels)
+    return tuple(fr) if isinstance(fr, (tuple, list)) else (fr,)
+
+
+def write_y4m(path, frames, width, height: Optional[int] = None, chroma: str = CHROMA_420,
+              frame_rate=(30, 1)) -> None:
+    """Write 8-bit frames as YUV4MPEG2: ``write_y4m(path, frames, header)`` as in the
+    reference (src/media.py:272-281), or with explicit width / height / chroma."""
+    if isinstance(width, StreamHeader):
+        hd = width
+        width, height, chroma, frame_rate = hd.width, hd.height, hd.chroma, hd.frame_rate
     tag = {CHROMA_420: "420jpeg", CHROMA_444: "444", "mono": "mono"}[chroma]
     with open(path, "wb") as fh:
         fh.write(Y4M_MAGIC + f" W{width} H{height} F{frame_rate[0]}:{frame_rate[1]} C{tag}\n".encode())
         for fr in frames:
             fh.write(b"FRAME\n")
-            for p in (fr if isinstance(fr, (tuple, list)) else (fr,)):
+            for p in _frame_planes(fr):
                 fh.write(np.ascontiguousarray(p, dtype=np.uint8).tobytes())
 
 
@@ -177,8 +199,161 @@ def write_planar_raw(path, frames, bit_depth: int = 8) -> None:
     dt = np.uint8 if bit_depth <= 8 else np.dtype("<u2")
     with open(path, "wb") as fh:
         for fr in frames:
-            for p in (fr if isinstance(fr, (tuple, list)) else (fr,)):
+            for p in _frame_planes(fr):
                 fh.write(np.ascontiguousarray(p, dtype=dt).tobytes())
+
+
+# ---------------------------------------------------------------------------
+# reference-named readers (src/media.py:58-237) over the memory-mapped sources
+# ---------------------------------------------------------------------------
+
+class VideoStream:
+    """Stream header plus frames (src/media.py:58-70); iterating yields LumaPlane for mono
+    streams and YCbCr ColorFrame otherwise, each a zero-copy view of the mapping."""
+
+    def __init__(self, source: FrameSource):
+        self.source = source
+        self.header = source.header
+
+    def __len__(self) -> int:
+        return len(self.source)
+
+    def frame(self, i: int):
+        planes = self.source.planes(i)
+        bd = self.header.bit_depth
+        if self.header.chroma == "mono":
+            return LumaPlane(planes[0], bd)
+        return ColorFrame(planes, SPACE_YCBCR, self.header.chroma, bd)
+
+    def __iter__(self):
+        for i in range(len(self.source)):
+            yield self.frame(i)
+
+    def luma_frames(self):
+        for y in self.source.luma():
+            yield LumaPlane(y, self.header.bit_depth)
+
+
+def read_y4m(path) -> VideoStream:
+    """Open a YUV4MPEG2 file (src/media.py:94-118)."""
+    return VideoStream(open_y4m(path))
+
+
+def read_planar_raw(path, width: int, height: int, bit_depth: int = 8, chroma: str = CHROMA_420,
+                    frame_rate=(30, 1)) -> VideoStream:
+    """Open a headerless planar YUV file; dimensions from the caller (src/media.py:178-212)."""
+    return VideoStream(open_raw(path, width, height, bit_depth, chroma, frame_rate))
+
+
+def read_pnm(path):
+    """Binary PNM (src/media.py:215-269): P5 -> LumaPlane, P6 -> RGB ColorFrame; 16-bit big-endian."""
+    with open(path, "rb") as fh:
+        data = fh.read()
+    if data[:2] not in (b"P5", b"P6"):
+        raise BadHeader(f"{path}: not a binary P5/P6 PNM file")
+    kind = data[:2].decode()
+    fields: list = []
+    i = 2
+    while len(fields) < 3:
+        if i >= len(data):
+            raise BadHeader(f"{path}: truncated PNM header")
+        c = data[i:i + 1]
+        if c == b"#":
+            while i < len(data) and data[i:i + 1] != b"\n":
+                i += 1
+        elif c.isspace():
+            i += 1
+        elif c.isdigit():
+            j = i
+            while j < len(data) and data[j:j + 1].isdigit():
+                j += 1
+            fields.append(int(data[i:j]))
+            i = j
+        else:
+            raise BadHeader(f"{path}: unexpected byte {c!r} in PNM header")
+    i += 1  # the single whitespace byte after maxval
+    width, height, maxval = fields
+    if width <= 0 or height <= 0:
+        raise BadHeader(f"{path}: bad dimensions {width}x{height}")
+    if maxval <= 0 or maxval > 65535:
+        raise UnsupportedMaxval(f"maxval {maxval} outside (0, 65535]")
+    bd = 8 if maxval <= 255 else 16
+    dt = np.dtype(np.uint8) if bd == 8 else np.dtype(">u2")
+    nch = 1 if kind == "P5" else 3
+    count = width * height * nch
+    payload = np.frombuffer(data, dtype=dt, count=min(count, (len(data) - i) // dt.itemsize), offset=i)
+    if payload.size < count:
+        raise TruncatedFrame(f"{path}: expected {count} samples, found {payload.size}")
+    if kind == "P5":
+        return LumaPlane(payload.reshape(height, width), bd)
+    rgb = payload.reshape(height, width, 3)
+    return ColorFrame((rgb[:, :, 0], rgb[:, :, 1], rgb[:, :, 2]), SPACE_RGB, CHROMA_444, bd)
+
+
+def open_stream(path, width: Optional[int] = None, height: Optional[int] = None, bit_depth: int = 8,
+                chroma: str = CHROMA_420):
+    """Any supported media file as a stream (src/pipeline.py:118-141); images -> 1-frame lists."""
+    ext = os.path.splitext(str(path))[1].lower()
+    if ext == ".y4m":
+        return read_y4m(path)
+    if ext in (".pnm", ".pgm", ".ppm"):
+        return [read_pnm(path)]
+    if width is None or height is None:
+        raise ValidationError(f"{path}: raw planar input needs explicit --width and --height")
+    return read_planar_raw(path, width, height, bit_depth, chroma)
+
+
+# ---------------------------------------------------------------------------
+# report writer (src/media.py:310-372): deterministic, byte-for-byte output
+# ---------------------------------------------------------------------------
+
+def format_float(x: float) -> str:
+    """9 significant digits, trailing zeros kept (1 -> 1.00000000)."""
+    return format(float(x), "#.9g")
+
+
+def _cell_csv(v) -> str:
+    if v is None:
+        return ""
+    if isinstance(v, bool):
+        return str(v).lower()
+    if isinstance(v, float):
+        return "" if v != v else format_float(v)
+    return str(v)
+
+
+def _cell_json(v) -> str:
+    import json
+
+    if v is None:
+        return "null"
+    if isinstance(v, bool):
+        return "true" if v else "false"
+    if isinstance(v, float):
+        return "null" if v != v else format_float(v)
+    if isinstance(v, int):
+        return str(v)
+    return json.dumps(str(v))
+
+
+def write_report(records, fmt: str = "jsonl", fields=None) -> bytes:
+    """Serialise per-frame records with a fixed field order (jsonl or csv)."""
+    import json
+
+    if fmt not in ("jsonl", "csv"):
+        raise ValidationError(f"unknown report format {fmt!r}")
+    if fields is None:
+        if not records:
+            raise ValidationError("empty record list needs an explicit field list")
+        fields = list(records[0].keys())
+    for i, rec in enumerate(records):
+        if set(rec.keys()) != set(fields):
+            raise ValidationError(f"record {i} does not match the report schema {list(fields)}")
+    if fmt == "csv":
+        lines = [",".join(fields)] + [",".join(_cell_csv(r[f]) for f in fields) for r in records]
+    else:
+        lines = ["{" + ", ".join(f"{json.dumps(f)}: {_cell_json(r[f])}" for f in fields) + "}" for r in records]
+    return ("\n".join(lines) + "\n").encode()
 
 
 def score_files(ref: FrameSource, dist: FrameSource, config=None, batch_frames: int = 16,

@@ -261,3 +261,101 @@ def _volume_score(volume, y1, y2, cfg: SsimConfig) -> FrameScore:
         mu1 = stats[:, 0]
     pooled, _ = pool_maps(terms[:, 2], pool, mu1)
     return FrameScore(float(pooled[0].item()), float(means[0]), float(means[1]), float(means[2]))
+
+
+# ---------------------------------------------------------------------------
+# whole-run driver (src/pipeline.py:261-366)
+# ---------------------------------------------------------------------------
+
+def _user_seconds() -> tuple[float, str]:
+    try:
+        import resource
+
+        return resource.getrusage(resource.RUSAGE_SELF).ru_utime, "user"
+    except ImportError:  # no resource module: wall time
+        import time
+
+        return time.perf_counter(), "wall"
+
+
+def run_score(ref_path, dist_path, spec: PipelineSpec, *, width: Optional[int] = None, height: Optional[int] = None,
+              bit_depth: int = 8, chroma: str = "420", batch_frames: int = 16) -> dict:
+    """Score two media files: {"records": per-frame dicts (FRAME_FIELDS), "summary": {...}}.
+
+    Luma pipelines over Y4M / raw streams run batched: memory-mapped planes ->
+    pinned double buffer -> device (``SequenceScorer``), ``batch_frames`` frames
+    per launch; SSIM-3D (kt > 1), the color models and still images go frame by
+    frame through ``score_frame_pair`` (all on the device).
+    """
+    import time
+
+    import numpy as np
+
+    from .errors import DimensionMismatch, LengthMismatch, SsimkitError
+    from .ingest import VideoStream, open_stream
+    from .planes import ScoreSeries
+    from .pooling import pool_temporal
+    from .volume import RollingVolume, msssim3d
+
+    ref = open_stream(ref_path, width, height, bit_depth, chroma)
+    dist = open_stream(dist_path, width, height, bit_depth, chroma)
+    if isinstance(ref, VideoStream) and isinstance(dist, VideoStream):
+        rh, dh = ref.header, dist.header
+        if (rh.width, rh.height) != (dh.width, dh.height):
+            raise DimensionMismatch(f"{ref_path} is {rh.width}x{rh.height}, {dist_path} is {dh.width}x{dh.height}")
+        if rh.bit_depth != dh.bit_depth or rh.chroma != dh.chroma:
+            raise DimensionMismatch("streams differ in bit depth or chroma subsampling")
+        if len(ref) != len(dist):
+            raise LengthMismatch(f"streams differ in length ({len(ref)} vs {len(dist)} frames)")
+    elif len(ref) != len(dist):
+        raise LengthMismatch("streams differ in length")
+    config = spec.config
+    start, timing_source = _user_seconds()
+    wall0 = time.perf_counter()
+    results: list = []
+    try:
+        batched = (spec.kt == 1 and config.color.model == "luma" and isinstance(ref, VideoStream)
+                   and isinstance(dist, VideoStream))
+        if batched:
+            from .video import SequenceScorer
+
+            cfg = config.for_bit_depth(ref.header.bit_depth)
+            seq = SequenceScorer(cfg, batch_frames).score(ref.source.luma(), dist.source.luma())
+            results = [FrameScore(r.score, r.am, r.l_mean, r.cs_mean) for r in seq.records]
+        elif spec.kt > 1 and config.multiscale.enabled:
+            series = msssim3d(_luma_iter(ref), _luma_iter(dist), spec.kt, config.multiscale, config)
+            results = [FrameScore(float(x), None, None, None) for x in series.scores]
+        else:
+            volume = RollingVolume(spec.kt) if spec.kt > 1 else None
+            for i, (a, b) in enumerate(zip(ref, dist)):
+                try:
+                    results.append(score_frame_pair(a, b, config, volume))
+                except SsimkitError as exc:
+                    raise type(exc)(f"frame {i}: {exc}") from exc
+    except SsimkitError as exc:
+        raise type(exc)(f"{ref_path} vs {dist_path}: {exc}") from exc
+    if not results:
+        raise ValidationError(f"{ref_path} vs {dist_path}: no frames to score")
+    end, _ = _user_seconds()
+    elapsed = end - start if timing_source == "user" else time.perf_counter() - wall0
+    records = [{"frame": i, "score": r.score, "am": r.am, "l_mean": r.l_mean, "cs_mean": r.cs_mean}
+               for i, r in enumerate(results)]
+    scores = np.array([r.score for r in results], dtype=np.float64)
+    summary = {"frames": len(results), "spatial_pool": config.spatial_pool, "temporal_pool": config.temporal_pool,
+               "pooled_score": pool_temporal(ScoreSeries(scores), config.temporal_pool),
+               "mean_score": float(scores.mean()), "user_seconds": elapsed, "timing_source": timing_source}
+    ams = [r.am for r in results if r.am is not None]
+    if ams:
+        summary["mean_am"] = float(np.mean(ams))
+    if parse_spatial(config.spatial_pool).kind == "cov":
+        summary["note"] = ("cov pooling maps a perfect (constant 1) quality map to 0; "
+                           "per-frame arithmetic means are reported in the 'am' field")
+    return {"records": records, "summary": summary}
+
+
+def _luma_iter(stream):
+    from .ingest import VideoStream
+
+    if isinstance(stream, VideoStream):
+        return stream.luma_frames()
+    return (_luma_plane(f) for f in stream)
