@@ -226,8 +226,11 @@ def run_reference(args) -> None:
     per_step = cores  # one pair per worker process per step
     pairs = cpu_pairs(per_step, cores)
     cpu = CpuBaseline(cores)
+    # warm-up steps run the same algorithm on 256x512 crops of the step's pairs (worker
+    # imports, allocator and caches warmed; a full 1080p step is ~12 s of CPU per pair)
+    crops = [(a[:256, :512].copy(), b[:256, :512].copy()) for a, b in pairs]
     for _ in range(args.warmup):
-        cpu.rate(pairs)
+        cpu.rate(crops)
     t_total = 0.0
     for _ in range(args.steps):
         _, wall = cpu.rate(pairs)
