@@ -79,6 +79,31 @@ def main() -> None:
     out["config5"] = {"pairs_per_s": n / sec, "TFLOPs": flops / sec / 1e12, "batch": n, "pool": 8,
                       "note": "4800 pairs would take %.3f s on one GPU" % (4800 / (n / sec))}
     del ref, dist
+    # the whole 4800-pair sweep resident in HBM (2 x 39.8 GB of 4K u8 frames), scored in
+    # 300-frame launches: per-frame SSIM + MS-SSIM scores only leave the device at the end
+    if "--no-sweep" not in sys.argv:
+        total, chunk = 4800, 300
+        big_r = torch.empty((total, 2160, 3840), dtype=torch.uint8, device=dev)
+        big_d = torch.empty_like(big_r)
+        pr = torch.from_numpy(np.stack([p[0] for p in pool])).to(dev)
+        pd = torch.from_numpy(np.stack([p[1] for p in pool])).to(dev)
+        for i in range(0, total, len(pool)):
+            big_r[i:i + len(pool)].copy_(pr)
+            big_d[i:i + len(pool)].copy_(pd)
+        del pr, pd
+
+        def sweep():
+            outs = [P.msssim_batch(big_r[i:i + chunk], big_d[i:i + chunk], cfg, spec, with_ssim=True)
+                    for i in range(0, total, chunk)]
+            return torch.cat([o[0] for o in outs]), torch.cat([o[1].score for o in outs])
+
+        sec = timed(sweep, 2)
+        ms_scores, ss_scores = sweep()
+        out["config5_resident_sweep"] = {
+            "pairs": total, "seconds": sec, "pairs_per_s": total / sec, "hbm_resident_GB": 2 * big_r.numel() / 1e9,
+            "msssim_mean": float(ms_scores.mean()), "ssim_mean": float(ss_scores.mean()), "chunk": chunk}
+        del big_r, big_d
+        torch.cuda.empty_cache()
 
     # enhanced preset (rect 11 stride 5, integral engine, dh:3 box downsampling, CoV pooling) at 1080p
     pool = [synth.dct_pair(2, i, 1080, 1920) for i in range(8)]
