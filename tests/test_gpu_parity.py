@@ -598,3 +598,24 @@ def test_score_files_y4m(cuda, oracle, tmp_path):
     assert np.max(np.abs(res.scores - np.array(want))) < 1e-5
     luma = ingest.score_files(ref, dist, cfg, batch_frames=3)
     assert np.max(np.abs(luma.scores - np.array([oracle.ssim_score(r[0], d[0], **win) for r, d in pairs]))) < 1e-5
+
+
+def test_4k_config5_properties(cuda):
+    """Config 5 at full size, through size-independent properties: unit score at identity,
+    exact ref/dist symmetry, and batch invariance (a frame's scores do not depend on its
+    batch neighbours) for Gaussian SSIM + 5-scale MS-SSIM on 3840x2160 u8."""
+    import torch
+    from paper_2101_06354_b200 import synth
+
+    pairs = [synth.dct_pair(5, i, 2160, 3840) for i in range(2)]
+    ref = torch.from_numpy(np.stack([pairs[0][0], pairs[1][0], pairs[0][0]])).to(cuda)
+    dist = torch.from_numpy(np.stack([pairs[0][1], pairs[1][1], pairs[0][0]])).to(cuda)
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    spec = P.MultiscaleSpec.product(5)
+    ms, terms = P.msssim_batch(ref, dist, cfg, spec, with_ssim=True)
+    ms_sw, terms_sw = P.msssim_batch(dist, ref, cfg, spec, with_ssim=True)
+    assert torch.equal(ms, ms_sw) and torch.equal(terms.score, terms_sw.score)  # exact symmetry
+    assert abs(float(ms[2]) - 1.0) < 1e-6 and abs(float(terms.score[2]) - 1.0) < 1e-6  # identity
+    alone, alone_t = P.msssim_batch(ref[1:2], dist[1:2], cfg, spec, with_ssim=True)
+    assert float(alone[0]) == float(ms[1]) and float(alone_t.score[0]) == float(terms.score[1])
+    assert 0.0 < float(ms[0]) < 1.0 and 0.0 < float(terms.score[0]) < 1.0
