@@ -28,6 +28,7 @@ struct PoolArgs {
   const unsigned char* aux;
   long long rp, fp, arp, afp;  // elements
   int n, h, w, nblk;           // nblk row ranges (blocks) per map
+  int flat;                    // rows contiguous (pitch == width) in values and aux: flat index loop
   double cnt;                  // h * w
   int kind;
   double p, o, a, b, ps, rs;
@@ -86,16 +87,33 @@ __device__ __forceinline__ double np_lerp(double lo, double hi, double t) {
   return t >= 0.5 ? __dsub_rn(hi, __dmul_rn(d, __dsub_rn(1.0, t))) : __dadd_rn(lo, __dmul_rn(d, t));
 }
 
-// Visit the elements of row range `blk` of one map: f(row, col), block-strided.
-template <int NT = PL_THREADS, typename F>
-__device__ __forceinline__ void for_range(const PoolArgs& a, int blk, F&& f) {
+// Visit the elements of row range `blk` of one map: f(load(value offset), value offset,
+// aux offset, slot 0..3), block-strided.  Contiguous maps (the usual [gh][gw] planes) take a flat
+// index loop that issues four independent loads before using any of them: one
+// outstanding load per thread leaves these streaming passes latency-bound.
+template <int NT = PL_THREADS, typename L, typename F>
+__device__ __forceinline__ void for_range(const PoolArgs& a, int blk, L&& load, F&& f) {
   const int r0 = (int)((long long)blk * a.h / a.nblk);
   const int r1 = (int)((long long)(blk + 1) * a.h / a.nblk);
+  if (a.flat) {
+    const long long e1 = (long long)r1 * a.w;
+    long long i = (long long)r0 * a.w + threadIdx.x;
+    for (; i + 3 * NT < e1; i += 4 * NT) {
+      const auto v0 = load(i), v1 = load(i + NT), v2 = load(i + 2 * NT), v3 = load(i + 3 * NT);
+      f(v0, i, i, 0);
+      f(v1, i + NT, i + NT, 1);
+      f(v2, i + 2 * NT, i + 2 * NT, 2);
+      f(v3, i + 3 * NT, i + 3 * NT, 3);
+    }
+    for (; i < e1; i += NT) f(load(i), i, i, 0);
+    return;
+  }
   const long long total = (long long)(r1 - r0) * a.w;
   const int dr = NT / a.w, dc = NT % a.w;
   int row = r0 + (int)(threadIdx.x / a.w), col = (int)(threadIdx.x % a.w);
   for (long long i = threadIdx.x; i < total; i += NT) {
-    f(row, col);
+    const long long vo = (long long)row * a.rp + col;
+    f(load(vo), vo, (long long)row * a.arp + col, 0);
     row += dr;
     col += dc;
     if (col >= a.w) {
@@ -103,12 +121,6 @@ __device__ __forceinline__ void for_range(const PoolArgs& a, int blk, F&& f) {
       ++row;
     }
   }
-}
-
-template <typename T>
-__device__ __forceinline__ double map_at(const unsigned char* base, long long fp, long long rp, int frame, int row,
-                                         int col) {
-  return (double)reinterpret_cast<const T*>(base)[(long long)frame * fp + (long long)row * rp + col];
 }
 
 __device__ __forceinline__ double warp_min(double v) {
@@ -138,9 +150,8 @@ __device__ double rank_value(const PoolArgs& a, int frame, int r) {
 
 // per-element work of the two passes
 template <typename T>
-__device__ __forceinline__ void pass1_elem(const PoolArgs& a, int frame, int row, int col, double& sum, double& mn,
-                                           double& mx, double& f1, double& f2) {
-  const double v = map_at<T>(a.vals, a.fp, a.rp, frame, row, col);
+__device__ __forceinline__ void pass1_elem(const PoolArgs& a, const T* ab, double v, long long ao, double& sum,
+                                           double& mn, double& mx, double& f1, double& f2) {
   sum += v;
   mn = fmin(mn, v);
   mx = fmax(mx, v);
@@ -151,21 +162,28 @@ __device__ __forceinline__ void pass1_elem(const PoolArgs& a, int frame, int row
   } else if (a.kind == SSK_POOL_MINK) {
     f1 += powp(__dsub_rn(1.0, v), a.p);
   } else if (a.kind == SSK_POOL_LW) {
-    const double mu = map_at<T>(a.aux, a.afp, a.arp, frame, row, col);
+    const double mu = (double)ab[ao];
     const double wt = a.b == 0.0 ? (mu >= a.a ? 1.0 : 0.0) : fmin(fmax(__ddiv_rn(__dsub_rn(mu, a.a), a.b), 0.0), 1.0);
     f1 += __dmul_rn(wt, v);
   }
 }
 
-template <typename T>
-__device__ __forceinline__ double pass2_elem(const PoolArgs& a, int frame, int row, int col, double c) {
-  const double v = map_at<T>(a.vals, a.fp, a.rp, frame, row, col);
+__device__ __forceinline__ double pass2_elem(const PoolArgs& a, double v, double c) {
   if (a.kind == SSK_POOL_COV) {
     const double d = __dsub_rn(v, c);
     return __dmul_rn(d, d);
   }
   if (a.kind == SSK_POOL_MD) return powp(fabs(__dsub_rn(v, c)), a.p);
   return v <= c ? __ddiv_rn(v, a.rs) : v;  // pp
+}
+
+template <typename T>
+__device__ __forceinline__ const T* frame_vals(const PoolArgs& a, int frame) {
+  return reinterpret_cast<const T*>(a.vals) + (long long)frame * a.fp;
+}
+template <typename T>
+__device__ __forceinline__ const T* frame_aux(const PoolArgs& a, int frame) {
+  return a.aux ? reinterpret_cast<const T*>(a.aux) + (long long)frame * a.afp : nullptr;
 }
 
 // pooled score from the folded sums (src/pooling.py:157-243 semantics)
@@ -219,8 +237,12 @@ __global__ void __launch_bounds__(PL_THREADS) pool_pass1_kernel(const __grid_con
     s[0] = 0ull;
     s[1] = (unsigned long long)a.rank[threadIdx.x];
   }
+  const T* vb = frame_vals<T>(a, frame);
+  const T* ab = frame_aux<T>(a, frame);
   double sum = 0.0, mn = INFINITY, mx = -INFINITY, f1 = 0.0, f2 = 0.0;
-  for_range(a, blk, [&](int row, int col) { pass1_elem<T>(a, frame, row, col, sum, mn, mx, f1, f2); });
+  for_range(
+      a, blk, [&](long long o) { return (double)vb[o]; },
+      [&](double v, long long, long long ao, int) { pass1_elem<T>(a, ab, v, ao, sum, mn, mx, f1, f2); });
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   sum = warp_sum(sum);
   mn = warp_min(mn);
@@ -262,7 +284,10 @@ __global__ void __launch_bounds__(PL_THREADS) pool_pass2_kernel(const __grid_con
   __syncthreads();
   const double c = centre_s;
   double acc = 0.0;
-  for_range(a, blk, [&](int row, int col) { acc += pass2_elem<T>(a, frame, row, col, c); });
+  const T* vb = frame_vals<T>(a, frame);
+  for_range(
+      a, blk, [&](long long o) { return (double)vb[o]; },
+      [&](double v, long long, long long, int) { acc += pass2_elem(a, v, c); });
   acc = warp_sum(acc);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
@@ -277,42 +302,85 @@ __global__ void __launch_bounds__(PL_THREADS) pool_pass2_kernel(const __grid_con
 // radix select: histogram of the next SEL_BITS-wide digit of the keys that
 // match each rank's prefix so far, then one block per map picks the digits
 // ---------------------------------------------------------------------------
+// Ranks whose key prefixes agree so far share one histogram (all of them in the first
+// pass): rep[r] = first rank with the same prefix above bit `hi`.
+template <typename K>
+__device__ __forceinline__ int prefix_rep(const unsigned long long* pre, int r, int hi, int bits) {
+  if (hi >= bits) return 0;
+  for (int q = 0; q < r; ++q)
+    if (((K)pre[q] >> hi) == ((K)pre[r] >> hi)) return q;
+  return r;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(PL_THREADS) select_hist_kernel(const __grid_constant__ PoolArgs a, int hi,
                                                                  int width) {
   extern __shared__ unsigned int sh[];  // [nranks][SEL_BINS]
   __shared__ unsigned long long pre[MAX_RANKS];
+  __shared__ int reps[MAX_RANKS], nrep;
   const int frame = blockIdx.y, blk = blockIdx.x;
-  const int nb = a.nranks * SEL_BINS;
-  for (int i = threadIdx.x; i < nb; i += PL_THREADS) sh[i] = 0u;
+  using K = typename Keys<T>::K;
   if ((int)threadIdx.x < a.nranks) pre[threadIdx.x] = a.sel[((long long)frame * MAX_RANKS + threadIdx.x) * 2];
   __syncthreads();
-  using K = typename Keys<T>::K;
+  if (threadIdx.x == 0) {
+    int m = 0;
+    for (int r = 0; r < a.nranks; ++r)
+      if (prefix_rep<K>(pre, r, hi, Keys<T>::B) == r) reps[m++] = r;
+    nrep = m;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nrep * SEL_BINS; i += PL_THREADS) sh[reps[i / SEL_BINS] * SEL_BINS + i % SEL_BINS] = 0u;
+  __syncthreads();
   const int shift = hi - width;
   const K mask = (K)((1u << width) - 1u);
   const bool first = hi >= Keys<T>::B;
-  const int nr = a.nranks;
-  for_range(a, blk, [&](int row, int col) {
-    const K key = Keys<T>::key(reinterpret_cast<const T*>(a.vals)[(long long)frame * a.fp + (long long)row * a.rp + col]);
+  const int nu = nrep;
+  const T* vb = frame_vals<T>(a, frame);
+  // quality maps crowd into a few leading digits (values near 1): when a whole warp's
+  // candidates fall into one bin, one shared atomic adds the warp's count
+  const unsigned lane = threadIdx.x & 31;
+  for_range(a, blk, [&](long long o) { return vb[o]; }, [&](T raw, long long, long long, int) {
+    const K key = Keys<T>::key(raw);
     const unsigned d = (unsigned)((key >> shift) & mask);
-    for (int r = 0; r < nr; ++r) {
-      if (first || (key >> hi) == ((K)pre[r] >> hi)) atomicAdd(&sh[r * SEL_BINS + d], 1u);
+    const unsigned active = __activemask();
+    const int leader = __ffs(active) - 1;
+    const unsigned d0 = __shfl_sync(active, d, leader);
+    for (int u = 0; u < nu; ++u) {
+      const int r = reps[u];
+      const bool hit = first || (key >> hi) == ((K)pre[r] >> hi);
+      const unsigned hits = __ballot_sync(active, hit);
+      if (!hits) continue;
+      if (__all_sync(active, !hit || d == d0)) {
+        if ((int)lane == leader) atomicAdd(&sh[r * SEL_BINS + d0], (unsigned)__popc(hits));
+      } else if (hit) {
+        atomicAdd(&sh[r * SEL_BINS + d], 1u);
+      }
     }
   });
   __syncthreads();
   unsigned int* g = a.hist + (long long)frame * MAX_RANKS * SEL_BINS;
-  for (int i = threadIdx.x; i < nb; i += PL_THREADS) {
-    const unsigned c = sh[i];
-    if (c) atomicAdd(&g[i], c);
+  for (int i = threadIdx.x; i < nrep * SEL_BINS; i += PL_THREADS) {
+    const int j = reps[i / SEL_BINS] * SEL_BINS + i % SEL_BINS;
+    const unsigned c = sh[j];
+    if (c) atomicAdd(&g[j], c);
   }
 }
 
-__global__ void __launch_bounds__(PL_THREADS) select_pick_kernel(const __grid_constant__ PoolArgs a, int shift) {
+template <typename T>
+__global__ void __launch_bounds__(PL_THREADS) select_pick_kernel(const __grid_constant__ PoolArgs a, int shift,
+                                                                 int hi) {
   __shared__ unsigned long long wtot[PL_THREADS / 32];
+  __shared__ unsigned long long pre[MAX_RANKS];
+  __shared__ int rep[MAX_RANKS];
   constexpr int PER = SEL_BINS / PL_THREADS;  // 8 bins per thread
   const int frame = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  // histogram owner of every rank, from the prefixes before this digit is appended
+  if (t < a.nranks) pre[t] = a.sel[((long long)frame * MAX_RANKS + t) * 2];
+  __syncthreads();
+  if (t < a.nranks) rep[t] = prefix_rep<typename Keys<T>::K>(pre, t, hi, Keys<T>::B);
+  __syncthreads();
   for (int r = 0; r < a.nranks; ++r) {
-    unsigned int* h = a.hist + ((long long)frame * MAX_RANKS + r) * SEL_BINS;
+    unsigned int* h = a.hist + ((long long)frame * MAX_RANKS + rep[r]) * SEL_BINS;
     unsigned long long* st = a.sel + ((long long)frame * MAX_RANKS + r) * 2;
     unsigned c[PER];
     unsigned long long s = 0;
@@ -346,10 +414,11 @@ __global__ void __launch_bounds__(PL_THREADS) select_pick_kernel(const __grid_co
         cum += c[j];
       }
     }
-#pragma unroll
-    for (int j = 0; j < PER; ++j) h[t * PER + j] = 0u;  // ready for the next digit
     __syncthreads();
   }
+  // clear every histogram for the next digit (shared ones are read by several ranks above)
+  for (int i = t; i < a.nranks * SEL_BINS; i += PL_THREADS)
+    a.hist[(long long)frame * MAX_RANKS * SEL_BINS + i] = 0u;
 }
 
 // ---------------------------------------------------------------------------
@@ -387,8 +456,12 @@ __global__ void __launch_bounds__(PS_THREADS) pool_small_kernel(const __grid_con
   __shared__ double tot[NC1];
   const int frame = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const T* vb = frame_vals<T>(a, frame);
+  const T* ab = frame_aux<T>(a, frame);
   double sum = 0.0, mn = INFINITY, mx = -INFINITY, f1 = 0.0, f2 = 0.0;
-  for_range<PS_THREADS>(a, 0, [&](int row, int col) { pass1_elem<T>(a, frame, row, col, sum, mn, mx, f1, f2); });
+  for_range<PS_THREADS>(
+      a, 0, [&](long long o) { return (double)vb[o]; },
+      [&](double v, long long, long long ao, int) { pass1_elem<T>(a, ab, v, ao, sum, mn, mx, f1, f2); });
   sum = warp_sum(sum);
   mn = warp_min(mn);
   mx = warp_max(mx);
@@ -414,7 +487,9 @@ __global__ void __launch_bounds__(PS_THREADS) pool_small_kernel(const __grid_con
   if (a.pass2) {
     const double c = __ddiv_rn(tot[0], a.cnt);
     double acc = 0.0;
-    for_range<PS_THREADS>(a, 0, [&](int row, int col) { acc += pass2_elem<T>(a, frame, row, col, c); });
+    for_range<PS_THREADS>(
+        a, 0, [&](long long o) { return (double)vb[o]; },
+        [&](double v, long long, long long, int) { acc += pass2_elem(a, v, c); });
     acc = warp_sum(acc);
     __syncthreads();
     if (lane == 0) red[warp][0] = acc;
@@ -661,6 +736,7 @@ int plan_pool(const ssk_maps* m, const ssk_pooler* pl, PoolPlan& P) {
   a.n = m->n;
   a.h = m->h;
   a.w = m->w;
+  a.flat = (m->row_pitch == m->w && (!m->aux || m->aux_row_pitch == m->w)) ? 1 : 0;
   const long long count = (long long)m->h * m->w;
   a.cnt = (double)count;
   // one block per map up to 32K samples (single-launch small-map path), else ~16K
@@ -731,10 +807,16 @@ int run_pool(PoolPlan& P, cudaStream_t st) {
     if (cudaFuncSetAttribute(select_hist_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return SSK_E_CUDA;
+    // histogram blocks cover ~64K samples each: every block zeroes and flushes whole
+    // 2048-bin histograms, so fewer, longer blocks amortise that fixed cost
+    PoolArgs as = a;
+    long long sb = ((long long)a.h * a.w + 65535) / 65536;
+    as.nblk = (int)(sb < 1 ? 1 : (sb > a.h ? a.h : sb));
+    const dim3 sgrid(as.nblk, a.n);
     for (int hi = B; hi > 0; hi -= SEL_BITS) {
       const int width = hi < SEL_BITS ? hi : SEL_BITS;
-      select_hist_kernel<T><<<grid, PL_THREADS, smem, st>>>(a, hi, width);
-      select_pick_kernel<<<a.n, PL_THREADS, 0, st>>>(a, hi - width);
+      select_hist_kernel<T><<<sgrid, PL_THREADS, smem, st>>>(as, hi, width);
+      select_pick_kernel<T><<<a.n, PL_THREADS, 0, st>>>(a, hi - width, hi);
       note_launch(2);
     }
   }
