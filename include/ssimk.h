@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SSK_ABI_VERSION 7
+#define SSK_ABI_VERSION 8
 
 /* sample storage types */
 enum {
@@ -315,6 +315,13 @@ size_t ssk_delta_e_workspace_bytes(int n, int h, int w);
 int ssk_delta_e(const ssk_color* ref, const ssk_color* dist, int smooth, int k, int stride, int mode, double* d_out,
                 int64_t out_row_pitch, int64_t out_frame_pitch, void* d_workspace, size_t workspace_bytes,
                 void* stream);
+
+/* Page-lock an existing host range (e.g. a memory-mapped media file) so frame planes
+ * are DMA'd straight to the device with no staging copy; read_only for read-only
+ * mappings.  0, or -1000 - cudaError_t when the driver refuses (the error is
+ * cleared, nothing else is affected). */
+int ssk_host_register(void* ptr, size_t bytes, int read_only);
+int ssk_host_unregister(void* ptr);
 
 /* Number of kernels this library has launched since load (for bench.py). */
 uint64_t ssk_launch_count(void);

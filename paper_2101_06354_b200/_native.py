@@ -32,7 +32,7 @@ RECT, GAUSS = 1, 2
 WANT_Q, WANT_L, WANT_CS, MAP_TERMS, MAP_STATS, WANT_Q2 = 1, 2, 4, 8, 16, 32
 E_ARG, E_WINDOW, E_SHAPE, E_WORKSPACE, E_ALIGN, E_CUDA, E_LEVELS, E_TOO_SMALL = range(-1, -9, -1)
 
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 EXPORTED_SYMBOLS = (
     "ssk_abi_version",
@@ -57,6 +57,8 @@ EXPORTED_SYMBOLS = (
     "ssk_qssim",
     "ssk_delta_e_workspace_bytes",
     "ssk_delta_e",
+    "ssk_host_register",
+    "ssk_host_unregister",
     "ssk_launch_count",
     "ssk_probe_fp32_tflops",
 )
@@ -214,6 +216,10 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         lib.ssk_delta_e.restype = i32
         lib.ssk_delta_e.argtypes = [pC, pC, i32, i32, i32, i32, vp, i64, i64, vp, sz, vp]
         del pD
+        lib.ssk_host_register.restype = i32
+        lib.ssk_host_register.argtypes = [vp, sz, i32]
+        lib.ssk_host_unregister.restype = i32
+        lib.ssk_host_unregister.argtypes = [vp]
         lib.ssk_launch_count.restype = ctypes.c_uint64
         lib.ssk_probe_fp32_tflops.restype = i32
         lib.ssk_probe_fp32_tflops.argtypes = [ctypes.c_double, ctypes.POINTER(ctypes.c_double), vp]

@@ -634,6 +634,26 @@ int ssk_volume_ssim(const ssk_volume* v, const ssk_window* win, int want, double
 
 uint64_t ssk_launch_count(void) { return g_launches.load(); }
 
+int ssk_host_register(void* ptr, size_t bytes, int read_only) {
+  if (!ptr || !bytes) return SSK_E_ARG;
+  const unsigned flags = cudaHostRegisterPortable | (read_only ? cudaHostRegisterReadOnly : 0u);
+  const cudaError_t e = cudaHostRegister(ptr, bytes, flags);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();  // not sticky: clear it so later launch checks do not see it
+    return -1000 - (int)e;     // SSK_E_CUDA family; the cudaError_t is recoverable for diagnostics
+  }
+  return SSK_OK;
+}
+
+int ssk_host_unregister(void* ptr) {
+  if (!ptr) return SSK_E_ARG;
+  if (cudaHostUnregister(ptr) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return SSK_E_CUDA;
+  }
+  return SSK_OK;
+}
+
 int ssk_probe_fp32_tflops(double seconds, double* tflops, void* stream) {
   if (!tflops || seconds <= 0) return SSK_E_ARG;
   return probe_fp32(seconds, tflops, static_cast<cudaStream_t>(stream));

@@ -68,9 +68,11 @@ class FrameSource:
         self.path = str(path)
         self.header = header
         self._offsets = list(offsets)
-        # np.memmap keeps the mapping alive for as long as any returned plane view exists
+        # np.memmap keeps the mapping alive for as long as any returned plane view exists; a
+        # private (copy-on-write) mapping, because the driver page-locks private mappings
+        # (pin) but refuses shared file mappings.  Nothing ever writes through it.
         size = os.path.getsize(self.path)
-        self._buf = np.memmap(self.path, dtype=np.uint8, mode="r") if size else np.zeros(0, np.uint8)
+        self._buf = np.memmap(self.path, dtype=np.uint8, mode="c") if size else np.zeros(0, np.uint8)
 
     def __len__(self) -> int:
         return len(self._offsets)
@@ -93,8 +95,32 @@ class FrameSource:
         for i in range(len(self)):
             yield self.planes(i)
 
+    @property
+    def pinned(self) -> bool:
+        return getattr(self, "_pinned", False)
+
+    def pin(self) -> bool:
+        """Page-lock the mapping (``ssk_host_register``) so the scorer DMAs frame
+        planes straight from the page cache with no staging copy.  False if the driver
+        refuses (the scorer then packs through its pinned buffers as usual)."""
+        if self.pinned or self._buf.size == 0:
+            return self.pinned
+        from . import _native as nat
+
+        nat.require_device()
+        self._pinned = nat.lib().ssk_host_register(self._buf.ctypes.data, self._buf.nbytes, 0) == 0
+        return self._pinned
+
+    def unpin(self) -> None:
+        if self.pinned:
+            from . import _native as nat
+
+            nat.lib().ssk_host_unregister(self._buf.ctypes.data)
+            self._pinned = False
+
     def close(self) -> None:
         """Drop this source's reference to the mapping (views handed out stay valid)."""
+        self.unpin()
         self._buf = np.zeros(0, np.uint8)
 
 
@@ -372,6 +398,7 @@ def score_files(ref: FrameSource, dist: FrameSource, config=None, batch_frames: 
         raise ValidationError(f"streams differ in length: {len(ref)} vs {len(dist)} frames")
     cfg = config.for_bit_depth(ref.header.bit_depth)
     scorer = SequenceScorer(cfg, batch_frames, color_weights)
+    direct = ref.pin() and dist.pin()  # page-locked mappings: planes DMA'd with no host copy
     if color_weights is not None:
-        return scorer.score(ref.frames(), dist.frames())
-    return scorer.score(ref.luma(), dist.luma())
+        return scorer.score(ref.frames(), dist.frames(), direct=direct)
+    return scorer.score(ref.luma(), dist.luma(), direct=direct)

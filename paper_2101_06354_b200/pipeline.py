@@ -320,7 +320,8 @@ def run_score(ref_path, dist_path, spec: PipelineSpec, *, width: Optional[int] =
             from .video import SequenceScorer
 
             cfg = config.for_bit_depth(ref.header.bit_depth)
-            seq = SequenceScorer(cfg, batch_frames).score(ref.source.luma(), dist.source.luma())
+            direct = ref.source.pin() and dist.source.pin()  # DMA straight from the page-locked mapping
+            seq = SequenceScorer(cfg, batch_frames).score(ref.source.luma(), dist.source.luma(), direct=direct)
             results = [FrameScore(r.score, r.am, r.l_mean, r.cs_mean) for r in seq.records]
         elif spec.kt > 1 and config.multiscale.enabled:
             series = msssim3d(_luma_iter(ref), _luma_iter(dist), spec.kt, config.multiscale, config)

@@ -19,6 +19,7 @@ scoring, in frame order.
 from __future__ import annotations
 
 import os
+import warnings
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 from typing import Iterable, Optional, Sequence
@@ -109,8 +110,12 @@ class SequenceScorer:
         self._done = [None, None]     # scoring of the slot finished (device buffer reusable)
 
     # -- staging ------------------------------------------------------------
-    def _stage(self, slot: int, frames: list):
-        """Pack a batch into pinned slot memory and upload it on the copy stream."""
+    def _stage(self, slot: int, frames: list, direct: bool = False):
+        """Pack a batch into pinned slot memory and upload it on the copy stream.
+
+        ``direct``: the frame planes already live in page-locked host memory (a pinned
+        ``FrameSource``); planes whose rows need no padding are then DMA'd straight into
+        the device slot, without the host packing copy."""
         torch = nat.torch_mod()
         nplanes = 3 if self.color_weights is not None else 1
         planes_ref, planes_dist = [], []
@@ -144,17 +149,29 @@ class SequenceScorer:
             # copies release the GIL, so the host memcpy runs on several cores), then
             # issue one async H2D per plane
             jobs = []
+            dma = []
             for p, (host, dev, w) in enumerate(slot_bufs[1]):
+                if direct and dev.shape[-1] == w:
+                    dma.append(p)
+                    continue
                 hv = host.numpy()
                 for i, (r, d) in enumerate(frames):
                     jobs.append((hv[0, i, :, :w], r[p] if nplanes == 3 else r))
                     jobs.append((hv[1, i, :, :w], d[p] if nplanes == 3 else d))
-            list(self._copier.map(_copy_into, jobs))
-            for p, (host, dev, w) in enumerate(slot_bufs[1]):
-                dev.copy_(host, non_blocking=True)
-                nbytes += host.numel() * host.element_size()
-                planes_ref.append(dev[0, :, :, :w])
-                planes_dist.append(dev[1, :, :, :w])
+            if jobs:
+                list(self._copier.map(_copy_into, jobs))
+            with warnings.catch_warnings():  # read-only mappings: torch only reads them
+                warnings.simplefilter("ignore", UserWarning)
+                for p, (host, dev, w) in enumerate(slot_bufs[1]):
+                    if p in dma:
+                        for i, (r, d) in enumerate(frames):
+                            dev[0, i].copy_(torch.from_numpy(r[p] if nplanes == 3 else r), non_blocking=True)
+                            dev[1, i].copy_(torch.from_numpy(d[p] if nplanes == 3 else d), non_blocking=True)
+                    else:
+                        dev.copy_(host, non_blocking=True)
+                    nbytes += dev.numel() * dev.element_size()
+                    planes_ref.append(dev[0, :, :, :w])
+                    planes_dist.append(dev[1, :, :, :w])
             ev = torch.cuda.Event()
             ev.record(self.copy_stream)
         self._events[slot] = ev
@@ -170,7 +187,9 @@ class SequenceScorer:
         rec = luma_records(pair, cfg, strict=False)
         return rec.score, rec
 
-    def score(self, ref_frames: Iterable, dist_frames: Iterable) -> SequenceResult:
+    def score(self, ref_frames: Iterable, dist_frames: Iterable, direct: bool = False) -> SequenceResult:
+        """Score two frame streams.  ``direct`` declares the planes page-locked
+        (``FrameSource.pin``), enabling copy-free DMA staging."""
         torch = nat.torch_mod()
         result = SequenceResult()
         pending = []
@@ -180,7 +199,7 @@ class SequenceScorer:
 
         def flush(frames):
             nonlocal slot
-            pr, pd, ev, nbytes = self._stage(slot, frames)
+            pr, pd, ev, nbytes = self._stage(slot, frames, direct)
             result.h2d_bytes += nbytes
             compute.wait_event(ev)
             score, terms = self._score_batch(pr, pd)
