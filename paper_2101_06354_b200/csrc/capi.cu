@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <utility>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -510,18 +511,28 @@ int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, const dou
       ++l;
       continue;
     }
+    // Longest tiles first (LPT): every frame pair's tiles of the tallest segments are
+    // dispatched before any shorter ones, so the short tiles of the small levels fill
+    // the last wave instead of trailing behind it.
+    int order[GS_MAX_LEVELS], nl = 0;
+    while (l < levels && nl < GS_MAX_LEVELS && plans[l].gauss && plans[l].ga.vcols == GS_THREADS) order[nl++] = l++;
+    for (int i = 1; i < nl; ++i)
+      for (int j = i; j > 0 && plans[order[j]].ga.seg_rows > plans[order[j - 1]].ga.seg_rows; --j)
+        std::swap(order[j], order[j - 1]);
     GaussLevels gl{};
-    int ctas = 0;
-    while (l < levels && gl.nlev < GS_MAX_LEVELS && plans[l].gauss && plans[l].ga.vcols == GS_THREADS) {
-      gl.lv[gl.nlev] = plans[l].ga;
-      gl.cta_off[gl.nlev] = ctas;
-      gl.nstrips[gl.nlev] = (int)plans[l].grid.x;
-      gl.nseg[gl.nlev] = (int)plans[l].grid.y;
-      ctas += (int)(plans[l].grid.x * plans[l].grid.y);
-      ++gl.nlev;
-      ++l;
+    gl.npairs = (p->n + 1) / 2;
+    long long ctas = 0;
+    for (int i = 0; i < nl; ++i) {
+      const Plan& pl = plans[order[i]];
+      gl.lv[i] = pl.ga;
+      gl.cta_off[i] = (int)ctas;
+      gl.nstrips[i] = (int)pl.grid.x;
+      gl.nseg[i] = (int)pl.grid.y;
+      ctas += (long long)pl.grid.x * pl.grid.y * gl.npairs;
     }
-    rc = launch_gauss_levels(gl, dim3(ctas, 1, (p->n + 1) / 2), win->k, gl.lv[0].dtype, st);
+    gl.nlev = nl;
+    if (ctas > 0x7fffffffLL) return SSK_E_ARG;
+    rc = launch_gauss_levels(gl, dim3((unsigned)ctas, 1, 1), win->k, gl.lv[0].dtype, st);
     if (rc) return rc;
   }
 

@@ -523,7 +523,9 @@ __global__ void __launch_bounds__(WS ? 2 * GS_THREADS : GS_THREADS, WS ? 2 : 4)
     if (i < p.nlev && (int)blockIdx.x >= p.cta_off[i]) lv = i;
   const int local = blockIdx.x - p.cta_off[lv];
   const int ns = p.nstrips[lv];
-  gauss_body<K, TIN, NM, WS, GS_THREADS>(p.lv[lv], local % ns, local / ns, blockIdx.z, ns, p.nseg[lv]);
+  const int ntiles = ns * p.nseg[lv];
+  const int pair = local / ntiles, tile = local - pair * ntiles;
+  gauss_body<K, TIN, NM, WS, GS_THREADS>(p.lv[lv], tile % ns, tile / ns, pair, ns, p.nseg[lv]);
 }
 
 template <int K, typename TIN, int NM, int VC = GS_THREADS, bool WS = true>

@@ -43,7 +43,8 @@ constexpr int GS_MAX_LEVELS = 4;  // pyramid levels fused into one multi-level l
 struct GaussLevels {
   GaussArgs lv[GS_MAX_LEVELS];
   int nlev;
-  int cta_off[GS_MAX_LEVELS];  // first blockIdx.x of each level
+  int npairs;                  // frame pairs (two frames per CTA)
+  int cta_off[GS_MAX_LEVELS];  // first blockIdx.x of each level (level-major, then pair, then tile)
   int nstrips[GS_MAX_LEVELS];
   int nseg[GS_MAX_LEVELS];
 };
