@@ -136,8 +136,8 @@ def device_pair(ref, dist, bit_depth: int, gauss: bool, scale_log2: int = 0) -> 
 # kernels
 # ---------------------------------------------------------------------------
 
-def _ptr(t) -> Optional[int]:
-    return None if t is None else t.data_ptr()
+def _ptr(t, row: int = 0) -> Optional[int]:
+    return None if t is None else t[row:].data_ptr()
 
 
 def grid_shape(h: int, w: int, k: int, s: int) -> tuple[int, int]:
@@ -177,9 +177,27 @@ def ssim(pair: DevicePair, window, c1: float, c2: float, want: int, stream=None)
     return sums, maps
 
 
+# Batches of at least this many frames run as two halves on two side streams, so the
+# last (partial) wave of each kernel of one half is filled by CTAs of the other half
+# (measured on 64 x 1080p: 1.007 -> 0.983 ms per MS-SSIM step).  Per-frame results
+# do not depend on the split (segmentation depends on the frame geometry only).
+SPLIT_MIN_FRAMES = 32
+_SIDE_STREAMS: dict = {}
+
+
+def _side_streams(device, count: int):
+    torch = nat.torch_mod()
+    key = device.index
+    have = _SIDE_STREAMS.get(key, [])
+    while len(have) < count:
+        have.append(torch.cuda.Stream(device=device))
+    _SIDE_STREAMS[key] = have
+    return have[:count]
+
+
 def msssim_levels(pair: DevicePair, window, c1: float, c2: float, levels: int,
-                  with_ssim: bool = False, spec=None, stream=None):
-    """Whole MS-SSIM pyramid in one library call.
+                  with_ssim: bool = False, spec=None, stream=None, split: Optional[int] = None):
+    """Whole MS-SSIM pyramid in one library call (two, on side streams, for large batches).
 
     Returns (level means [n, levels] (cs below the coarsest, q at it), combined
     score [n] or None (when ``spec`` is given), level-0 SSIM means (q, l, cs)
@@ -188,7 +206,6 @@ def msssim_levels(pair: DevicePair, window, c1: float, c2: float, levels: int,
     torch = nat.torch_mod()
     lib = nat.lib()
     n, h, w = pair.shape
-    planes = pair.planes()
     win = nat.make_window(window, c1, c2)
     dev = pair.ref.device
     means = torch.empty((n, levels), dtype=torch.float64, device=dev)
@@ -201,11 +218,32 @@ def msssim_levels(pair: DevicePair, window, c1: float, c2: float, levels: int,
         e = spec.effective_exponents()
         exps = (ctypes.c_double * len(e))(*e)
         agg = 2 if spec.aggregation == "sum" else 1
-    ws_bytes = lib.ssk_msssim_workspace_bytes(ctypes.byref(planes), ctypes.byref(win), levels)
-    ws = nat.WORKSPACE.get(max(ws_bytes, 256), dev, stream)
-    rc = lib.ssk_msssim(ctypes.byref(planes), ctypes.byref(win), levels, exps, agg, means.data_ptr(),
-                        _ptr(scores), _ptr(ssim_sums), ws.data_ptr(), ws.numel(), nat.stream_handle(stream))
-    nat.raise_for(rc, "msssim")
+
+    def run(part: DevicePair, lo: int, st) -> None:
+        planes = part.planes()
+        ws_bytes = lib.ssk_msssim_workspace_bytes(ctypes.byref(planes), ctypes.byref(win), levels)
+        ws = nat.WORKSPACE.get(max(ws_bytes, 256), dev, st)
+        rc = lib.ssk_msssim(ctypes.byref(planes), ctypes.byref(win), levels, exps, agg,
+                            means[lo:].data_ptr(), _ptr(scores, lo), _ptr(ssim_sums, lo), ws.data_ptr(), ws.numel(),
+                            nat.stream_handle(st))
+        nat.raise_for(rc, "msssim")
+
+    parts = split if split is not None else (2 if n >= SPLIT_MIN_FRAMES else 1)
+    parts = max(1, min(int(parts), n))
+    if parts == 1:
+        run(pair, 0, stream)
+        return means, scores, ssim_sums
+    caller = stream if stream is not None else torch.cuda.current_stream(dev)
+    ready = torch.cuda.Event()
+    ready.record(caller)
+    bounds = [round(i * n / parts) for i in range(parts + 1)]
+    sides = _side_streams(dev, parts)
+    for i, side in enumerate(sides):
+        lo, hi = bounds[i], bounds[i + 1]
+        side.wait_event(ready)  # inputs and outputs were produced / allocated on the caller's stream
+        run(DevicePair(pair.ref[lo:hi], pair.dist[lo:hi], pair.code, pair.bit_depth, pair.scale_log2), lo, side)
+    for side in sides:
+        caller.wait_stream(side)
     return means, scores, ssim_sums
 
 

@@ -236,6 +236,34 @@ def test_batch_matches_per_pair(cuda, rng):
     assert np.array_equal(P.ssim_batch(ta, tb, cfg).cpu().numpy(), got)
 
 
+@pytest.mark.parametrize("n", [2, 7, 40])
+def test_msssim_side_stream_split_is_bit_identical(cuda, rng, n):
+    """Large batches run as sub-batches on side streams (engine.SPLIT_MIN_FRAMES); every
+    split gives the same bits as one launch sequence, on the caller's stream order."""
+    import torch
+
+    h, w = 96, 200
+    a = rng.integers(0, 256, (n, h, w)).astype(np.uint8)
+    b = np.clip(a.astype(int) + rng.integers(-25, 26, a.shape), 0, 255).astype(np.uint8)
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    pair = engine.device_pair(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), 8, gauss=True)
+    spec = P.MultiscaleSpec.product(3)
+    outs = []
+    for split in (1, 2, 3):
+        means, score, sums = engine.msssim_levels(pair, cfg.window, cfg.c1, cfg.c2, 3, with_ssim=True,
+                                                  spec=spec, split=split)
+        outs.append([t.cpu().numpy() for t in (means, score, sums)])
+    for other in outs[1:]:
+        for x, y in zip(outs[0], other):
+            assert np.array_equal(x, y)
+    # the default (split when n >= SPLIT_MIN_FRAMES) agrees as well, on a user stream
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ms = P.msssim_batch(pair.ref, pair.dist, cfg, spec)
+    torch.cuda.synchronize()
+    assert np.array_equal(ms.cpu().numpy(), outs[0][1])
+
+
 def test_full_1080p_gauss_ssim_and_msssim(cuda, oracle):
     from paper_2101_06354_b200 import synth
 
