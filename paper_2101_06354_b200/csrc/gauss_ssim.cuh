@@ -87,6 +87,11 @@ __device__ __forceinline__ u64 add_rn2(u64 a, u64 b) {  // two IEEE scalar adds,
   upk(b, b0, b1);
   return pk(__fadd_rn(a0, b0), __fadd_rn(a1, b1));
 }
+__device__ __forceinline__ u64 maxc_2(u64 v, float c) {
+  float a, b;
+  upk(v, a, b);
+  return pk(fmaxf(a, c), fmaxf(b, c));
+}
 __device__ __forceinline__ u64 max0_2(u64 v) {
   float a, b;
   upk(v, a, b);
@@ -218,7 +223,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
   const u64 bias2 = pk(a.conv_bias, a.conv_bias);
   const u64 shift2 = pk(a.shift, a.shift);
   const u64 c1_2 = pk(a.c1, a.c1), c2_2 = pk(a.c2, a.c2);
-  const u64 two2 = pk(2.f, 2.f), one2 = pk(1.f, 1.f);
+  const u64 two2 = pk(2.f, 2.f), one2 = pk(1.f, 1.f), mtwo2 = pk(-2.f, -2.f);
   const u64 twoshift2 = pk(2.f * a.shift, 2.f * a.shift);
   const float c1b = 2.f * a.shift * a.shift + a.c1;  // 2 s^2 + C1 (exact for s = 2^(bd-1))
   const u64 c1b_2 = pk(c1b, c1b);
@@ -342,8 +347,10 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
       u64 acc[NM][8];
 #pragma unroll
       for (int m = 0; m < NM; ++m) {
+        // NM = 4: E[x^2 + y^2] starts at C2, so the filter itself yields
+        // sigma1^2 + sigma2^2 + C2 before the clamp (one add per output less)
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) acc[m][jj] = 0ull;
+        for (int jj = 0; jj < 8; ++jj) acc[m][jj] = (NM == 4 && m == 2) ? c2_2 : 0ull;
         const u64* vr = reinterpret_cast<const u64*>(vbuf + (m * G + hg) * VP + hj * 64);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
@@ -364,15 +371,21 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
         // Everything below is symmetric in (ref, dist): Pm = m1 m2, Sm = m1 + m2 and
         // Mm = m1^2 + m2^2 (IEEE scalar ops) are, and every further step uses only them.
         const u64 Pm = mul2(m1, m2);
-        const u64 nm2 = sub2(0ull, m2);  // exact negation; cov = fma(m1, -m2, E[xy]) stays one rounding
-        u64 v1, v2, cv, den2, Mm = 0ull;
+        // exact negation by flipping the sign bits (ALU pipe, not an FMA-pipe subtract);
+        // cov = fma(m1, -m2, E[xy]) stays one rounding
+        const u64 nm2 = m2 ^ 0x8000000080000000ull;
+        u64 v1, v2, cv, den2, Mm = 0ull, Sm = 0ull;
         if constexpr (NM == 4) {
-          // sigma1^2 + sigma2^2 = E[x^2 + y^2] - (m1^2 + m2^2), clamped as a sum
-          Mm = sumsq2(m1, m2);
-          v1 = max0_2(sub2(acc[2][jj], Mm));
+          // sigma1^2 + sigma2^2 = E[x^2 + y^2] - (m1^2 + m2^2), clamped as a sum:
+          // den2 = max(E[x^2 + y^2] + C2 - Mm, C2) with C2 carried by the filter
+          // m1^2 + m2^2 = Sm^2 - 2 m1 m2 from the symmetric Sm = m1 + m2 and Pm (one FMUL2 +
+          // one FFMA2 instead of six scalar ops; same error order as rounding m1^2 and m2^2)
+          Sm = add2(m1, m2);
+          Mm = fma2(Sm, Sm, mul2(Pm, mtwo2));
+          v1 = maxc_2(sub2(acc[2][jj], Mm), a.c2);
           v2 = 0ull;
           cv = fma2(m1, nm2, acc[3][jj]);
-          den2 = add2(v1, c2_2);
+          den2 = v1;
         } else {
           v1 = max0_2(sub2(acc[2][jj], mul2(m1, m1)));
           v2 = max0_2(sub2(acc[3][jj], mul2(m2, m2)));
@@ -385,8 +398,11 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
         if (full_terms) {
           // with mu = m + s (s = L/2): 2 mu1 mu2 + C1 = 2 Pm + T and mu1^2 + mu2^2 + C1 = Mm + T,
           // T = 2 s Sm + 2 s^2 + C1 (no catastrophic cancellation: all terms share a sign)
-          if constexpr (NM != 4) Mm = sumsq2(m1, m2);
-          const u64 T = fma2(twoshift2, add2(m1, m2), c1b_2);
+          if constexpr (NM != 4) {
+            Mm = sumsq2(m1, m2);
+            Sm = add2(m1, m2);
+          }
+          const u64 T = fma2(twoshift2, Sm, c1b_2);
           const u64 num1 = fma2(two2, Pm, T);
           const u64 den1 = add2(Mm, T);
           l = mul2(num1, rcp2(den1));
