@@ -24,6 +24,24 @@ int gauss_ws_level() {
   }();
   return v;
 }
+int gauss_persist_level() {
+  static const int v = [] {
+    const char* e = std::getenv("SSK_GAUSS_PERSIST");  // persistent wide u8 K1 (default on; 0 = one tile per CTA)
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cached[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n > 0 ? n : 148;
+  }
+  return cached[dev];
+}
 }  // namespace gk
 
 static std::atomic<unsigned long long> g_launches{0};

@@ -33,6 +33,7 @@
 // stride, so strided grids equal dense[::s, ::s] bit-exactly
 // (tests/test_stats.py:274-285).
 #pragma once
+#include <algorithm>
 #include <type_traits>
 
 #include "common.cuh"
@@ -153,8 +154,8 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-template <int K, typename TIN, int NM, bool WS, int VC>
-__device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, const int seg, const int pair,
+template <int K, typename TIN, int NM, bool WS, int VC, bool PERSIST = false>
+__device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0, const int seg0, const int pair0,
                                            const int nstrips, const int nseg) {
   constexpr int VP = vp_of(VC);
   constexpr int TW = tw_of(K, VC);
@@ -178,18 +179,31 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
   __shared__ double s_red[(2 * VC / 32) * 6];
 
   const int tid = threadIdx.x;
-  const int f0 = 2 * pair;
-  const bool has1 = f0 + 1 < a.n;
-  const int f1 = has1 ? f0 + 1 : f0;
-  const int c0 = strip * TW;
-  const int y0 = seg * a.seg_rows;
-  const int y1 = min(y0 + a.seg_rows, a.ho);
-  const int in_end = y1 + K - 1;
-  const int nchunks = (y1 - y0 + G - 1) / G;
-
-  // staged images: 0 = ref f0, 1 = ref f1, 2 = dist f0, 3 = dist f1
-  const long long fo0 = (long long)f0 * a.frame_pitch_b, fo1 = (long long)f1 * a.frame_pitch_b;
-  const int row_bytes_left = (a.w - c0) * ES;
+  // the tile (strip, segment, frame pair) being processed; a persistent CTA walks several
+  int strip, seg, f0, f1, c0, y0, y1, in_end, nchunks, own_end, row_bytes_left;
+  bool has1;
+  long long fo0, fo1;  // staged images: 0 = ref f0, 1 = ref f1, 2 = dist f0, 3 = dist f1
+  auto set_tile = [&](const int st, const int sg, const int pr) {
+    strip = st;
+    seg = sg;
+    f0 = 2 * pr;
+    has1 = f0 + 1 < a.n;
+    f1 = has1 ? f0 + 1 : f0;
+    c0 = st * TW;
+    y0 = sg * a.seg_rows;
+    y1 = min(y0 + a.seg_rows, a.ho);
+    in_end = y1 + K - 1;
+    nchunks = (y1 - y0 + G - 1) / G;
+    own_end = sg == nseg - 1 ? a.h : y1;
+    fo0 = (long long)f0 * a.frame_pitch_b;
+    fo1 = (long long)f1 * a.frame_pitch_b;
+    row_bytes_left = (a.w - c0) * ES;
+  };
+  const int npairs = (a.n + 1) / 2;
+  const int ntiles = nstrips * nseg * npairs;
+  auto tile_of = [&](const int t) { set_tile(t % nstrips, (t / nstrips) % nseg, t / (nstrips * nseg)); };
+  if constexpr (PERSIST) tile_of(blockIdx.x);
+  else set_tile(strip0, seg0, pair0);
 
   auto stage_rows = [&](int r_lo, int r_hi) {  // issued by the VC V-pass threads
     r_hi = min(r_hi, in_end);
@@ -212,7 +226,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
     cp_async_commit();
   };
 
-  if (tid < VC) stage_rows(y0, y0 + G + K - 1);
+  if (tid < VC) stage_rows(y0, y0 + G + K - 1);  // (persistent CTAs: their first tile)
   if (tid < 32) s_taps[tid] = a.taps[tid];
   __syncthreads();
   u64 w2[NH];
@@ -296,8 +310,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
   // staged rows [y0 + cG, y0 + (c+1)G) -- all remaining owned rows at the last
   // chunk -- into 2x2 block sums, exactly what pyramid_kernel writes for level 1.
   auto level1 = [&](const int c) {
-    const bool last_seg = seg == nseg - 1, last_strip = strip == nstrips - 1;
-    const int own_end = last_seg ? a.h : y1;
+    const bool last_strip = strip == nstrips - 1;
     const int rlo = y0 + c * G;
     const int rhi = (c == nchunks - 1) ? own_end : min(rlo + G, own_end);
     const int yb = rlo >> 1, ye = min(rhi >> 1, a.l1_h);
@@ -469,7 +482,74 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip, 
     constexpr int NB = nbuf_of(VC, ES);
     // NB V tiles in flight; named barriers 2..2+NB-1 = "tile b full",
     // 2+NBUF.. = "tile b free"; barrier 1 = producer-internal
-    if (tid < VC) {  // producers
+    if constexpr (PERSIST) {
+      // Persistent CTA (one per SM): tiles blockIdx.x, + gridDim.x, ...; the V-tile ring and
+      // its barriers run on across tile boundaries, so the producers stage and filter the
+      // next tile while the consumers drain the previous one (no per-tile fill / drain).
+      int total = 0;  // chunks this CTA will run (matches the consumers' "free" arrivals)
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int sg = (t / nstrips) % nseg;
+        total += (min((sg + 1) * a.seg_rows, a.ho) - sg * a.seg_rows + G - 1) / G;
+      }
+      int b = 0, cc = 0;
+      if (tid < VC) {  // producers
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+          if (t != (int)blockIdx.x) {
+            tile_of(t);
+            stage_rows(y0, y0 + G + K - 1);  // the previous tile's raw rows are no longer read
+          }
+          for (int c = 0; c < nchunks; ++c, ++cc) {
+            if (c + 1 < nchunks) {
+              stage_rows(y0 + (c + 1) * G + K - 1, y0 + (c + 2) * G + K - 1);
+              cp_async_wait<1>();
+            } else {
+              cp_async_wait<0>();
+            }
+            named_sync(1, VC);
+            if constexpr (VC == 256 && ES == 1) {
+              if (a.l1_ref) level1(c);
+            }
+            if (cc >= NB) named_sync(2 + NB + b, 2 * VC);
+            vpass(c, vbuf0 + b * VBYTES);
+            named_arrive(2 + b, 2 * VC);
+            named_sync(1, VC);
+            b = b + 1 == NB ? 0 : b + 1;
+          }
+        }
+      } else {  // consumers: H pass + epilogue, one partial triple per frame and tile
+        constexpr int CB = 2 + 2 * NB;  // consumer-internal barrier
+        const int cw = (tid - VC) >> 5;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+          if (t != (int)blockIdx.x) tile_of(t);
+          tq0 = tl0 = tc0 = tq1 = tl1 = tc1 = 0.0;
+          for (int c = 0; c < nchunks; ++c, ++cc) {
+            named_sync(2 + b, 2 * VC);
+            hpass(c, vbuf0 + b * VBYTES);
+            if (cc + NB < total) named_arrive(2 + NB + b, 2 * VC);
+            b = b + 1 == NB ? 0 : b + 1;
+          }
+          double v[6] = {tq0, tl0, tc0, tq1, tl1, tc1};
+#pragma unroll
+          for (int i = 0; i < 6; ++i) v[i] = warp_sum(v[i]);
+          if ((tid & 31) == 0) {
+#pragma unroll
+            for (int i = 0; i < 6; ++i) s_red[cw * 6 + i] = v[i];
+          }
+          named_sync(CB, VC);
+          const int ct = tid - VC;
+          if (ct < 6 && (ct < 3 || has1)) {
+            double acc = 0.0;
+#pragma unroll
+            for (int wi = 0; wi < VC / 32; ++wi) acc += s_red[wi * 6 + ct];
+            const int fr = ct < 3 ? f0 : f1;
+            const long long part = ((long long)fr * nseg + seg) * nstrips + strip;
+            a.partials[part * 3 + (ct % 3)] = acc;
+          }
+          named_sync(CB, VC);  // s_red is rewritten by the next tile
+        }
+      }
+      return;
+    } else if (tid < VC) {  // producers
       int b = 0;
       for (int c = 0; c < nchunks; ++c) {
         if (c + 1 < nchunks) {
@@ -527,6 +607,13 @@ __global__ void __launch_bounds__(2 * VC, VC == 128 ? 2 : 1) gauss_ws_kernel(con
   gauss_body<K, TIN, NM, true, VC>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.x, gridDim.y);
 }
 
+// Persistent variant (one CTA per SM walking tiles blockIdx.x, + gridDim.x, ...)
+template <int K, typename TIN, int NM, int VC>
+__global__ void __launch_bounds__(2 * VC, 1)
+    gauss_ws_persist_kernel(const __grid_constant__ GaussArgs a, const int nstrips, const int nseg) {
+  gauss_body<K, TIN, NM, true, VC, true>(a, 0, 0, 0, nstrips, nseg);
+}
+
 // All pyramid levels of one sample type in one launch: blockIdx.x enumerates the
 // (level, segment, strip) tiles, so the small coarse levels share the GPU with
 // each other instead of each launching a few dozen CTAs.
@@ -552,11 +639,27 @@ inline size_t smem_bytes() {
   return (size_t)RR * 4 * RB + (size_t)NM * G * vp_of(VC);
 }
 
+int gauss_persist_level();                    // capi.cu: SSK_GAUSS_PERSIST switch (default 1)
+int sm_count();                               // capi.cu: SMs of the current device
+
 template <int K, typename TIN, int NM, int VC>
 int launch_ws(const GaussArgs& a, dim3 grid, cudaStream_t st) {
-  auto fn = gauss_ws_kernel<K, TIN, NM, VC>;
   const size_t smem = smem_bytes<K, TIN, NM, VC>() +
                       (size_t)(nbuf_of(VC, (int)sizeof(TIN)) - 1) * NM * G * vp_of(VC);  // extra V tiles
+  if constexpr (VC == 256 && sizeof(TIN) == 1) {
+    // wide u8 strips (1 CTA / SM): persistent CTAs keep the V-tile pipeline full across tiles
+    const long long ntiles = (long long)grid.x * grid.y * grid.z;
+    if (gauss_persist_level() >= 1 && ntiles > 0) {
+      auto fp = gauss_ws_persist_kernel<K, TIN, NM, VC>;
+      if (cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return SSK_E_CUDA;
+      const int nctas = (int)std::min<long long>(ntiles, (long long)sm_count());
+      fp<<<nctas, 2 * VC, smem, st>>>(a, (int)grid.x, (int)grid.y);
+      note_launch();
+      return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+    }
+  }
+  auto fn = gauss_ws_kernel<K, TIN, NM, VC>;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SSK_E_CUDA;
   fn<<<grid, 2 * VC, smem, st>>>(a);
