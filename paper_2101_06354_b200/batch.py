@@ -142,6 +142,13 @@ class HostBatchScorer:
         Returns float64 numpy arrays: ``msssim`` -> [n]; ``ssim`` -> [n, 3]
         (score, l_mean, cs_mean); ``both`` -> ([n], [n, 3]).
         """
+        return self.submit(ref_host, dist_host).result()
+
+    def submit(self, ref_host, dist_host) -> "PendingScores":
+        """Queue one batch without waiting for it: uploads, kernels and the score read-back
+        are enqueued and a handle is returned whose ``result()`` waits for this batch only.
+        A stream of batches submitted one ahead keeps the copy engine busy across batches
+        (the next batch's uploads overlap this batch's last chunk and read-back)."""
         torch = nat.torch_mod()
         n = ref_host.shape[0]
         compute = torch.cuda.current_stream(self.device)
@@ -174,11 +181,37 @@ class HostBatchScorer:
             fin = torch.cuda.Event()
             fin.record(compute)
             done[0] = fin
-        ms_host = torch.cat(outs_ms).cpu().numpy() if outs_ms else None
-        ss_host = torch.cat(outs_ss).cpu().numpy() if outs_ss else None
-        self.d2h_bytes = (0 if ms_host is None else ms_host.nbytes) + (0 if ss_host is None else ss_host.nbytes)
+
+        def to_host(outs):
+            if not outs:
+                return None
+            dev = torch.cat(outs)
+            host = torch.empty(dev.shape, dtype=dev.dtype, pin_memory=True)
+            host.copy_(dev, non_blocking=True)
+            return host
+
+        ms_host, ss_host = to_host(outs_ms), to_host(outs_ss)
+        ready = torch.cuda.Event()
+        ready.record(compute)
+        self.d2h_bytes = sum(0 if t is None else t.numel() * t.element_size() for t in (ms_host, ss_host))
+        return PendingScores(self.mode, ms_host, ss_host, ready)
+
+
+class PendingScores:
+    """Scores of a submitted batch (``HostBatchScorer.submit``); ``result()`` waits for them."""
+
+    def __init__(self, mode: str, ms_host, ss_host, ready):
+        self.mode, self._ms, self._ss, self._ready = mode, ms_host, ss_host, ready
+
+    def done(self) -> bool:
+        return self._ready.query()
+
+    def result(self):
+        self._ready.synchronize()
+        ms = None if self._ms is None else self._ms.numpy()
+        ss = None if self._ss is None else self._ss.numpy()
         if self.mode == "msssim":
-            return ms_host
+            return ms
         if self.mode == "ssim":
-            return ss_host
-        return ms_host, ss_host
+            return ss
+        return ms, ss

@@ -465,6 +465,18 @@ def test_host_batch_scorer_matches_device_batch(cuda, rng):
     assert np.array_equal(ms, ms_dev.cpu().numpy())
     assert np.array_equal(ss[:, 0], terms.score.cpu().numpy())
     assert scorer.h2d_bytes == 2 * a.nbytes
+    # submitted one batch ahead (the bench's e2e loop): different batches in flight on the
+    # shared double-buffered chunks still score exactly like the synchronous call
+    batches = [(np.roll(a, i, axis=0), np.roll(b, i, axis=0)) for i in range(4)]
+    pend, got = None, []
+    for ra, rb in batches:
+        nxt = scorer.submit(torch.from_numpy(ra).pin_memory(), torch.from_numpy(rb).pin_memory())
+        if pend is not None:
+            got.append(pend.result())
+        pend = nxt
+    got.append(pend.result())
+    for i, (gms, gss) in enumerate(got):
+        assert np.array_equal(gms, np.roll(ms, i)) and np.array_equal(gss, np.roll(ss, i, axis=0))
 
 
 def test_sequence_scorer_multiscale_and_temporal_pooler(cuda, oracle, rng):
