@@ -137,7 +137,8 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
       return e ? std::atoi(e) : 0;
     }();
     const bool wide_ok = p->dtype == SSK_U8 || (p->dtype == SSK_U16 && wide_u16);
-    a.vcols = (gk::gauss_ws_level() >= 1 && wide_ok && k <= 17 && a.wo >= 480) ? 256 : 128;
+    const bool maps = (want & (SSK_MAP_TERMS | SSK_MAP_STATS)) != 0;  // maps: classic kernel only
+    a.vcols = (gk::gauss_ws_level() >= 1 && wide_ok && !maps && k <= 17 && a.wo >= 480) ? 256 : 128;
     const int tw = gauss_tw(k, a.vcols);
     const int nstrips = (a.wo + tw - 1) / tw;
     // Segments depend on the frame geometry only (never on the batch size), so a

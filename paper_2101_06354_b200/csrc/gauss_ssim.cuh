@@ -154,7 +154,8 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-template <int K, typename TIN, int NM, bool WS, int VC, bool PERSIST = false>
+// MAPS = false compiles the map stores out (score-only kernels: smaller code, no dead branches)
+template <int K, typename TIN, int NM, bool WS, int VC, bool PERSIST = false, bool MAPS = true>
 __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0, const int seg0, const int pair0,
                                            const int nstrips, const int nseg) {
   constexpr int VP = vp_of(VC);
@@ -242,7 +243,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
   const float c1b = 2.f * a.shift * a.shift + a.c1;  // 2 s^2 + C1 (exact for s = 2^(bd-1))
   const u64 c1b_2 = pk(c1b, c1b);
   const bool full_terms = (a.want & (SSK_WANT_Q | SSK_WANT_L)) != 0;
-  const bool want_maps = (a.want & (SSK_MAP_TERMS | SSK_MAP_STATS)) != 0;
+  const bool want_maps = MAPS && (a.want & (SSK_MAP_TERMS | SSK_MAP_STATS)) != 0;
   const int s = a.stride;
   const int wo = a.wo;
   const bool exact_sq = a.exact_sq != 0;
@@ -611,6 +612,7 @@ __global__ void __launch_bounds__(2 * VC, VC == 128 ? 2 : 1) gauss_ws_kernel(con
 template <int K, typename TIN, int NM, int VC>
 __global__ void __launch_bounds__(2 * VC, 1)
     gauss_ws_persist_kernel(const __grid_constant__ GaussArgs a, const int nstrips, const int nseg) {
+  // (the map branch stays compiled in: measured faster here than the MAPS = false build)
   gauss_body<K, TIN, NM, true, VC, true>(a, 0, 0, 0, nstrips, nseg);
 }
 
@@ -628,7 +630,7 @@ __global__ void __launch_bounds__(WS ? 2 * GS_THREADS : GS_THREADS, WS ? 2 : 4)
   const int ns = p.nstrips[lv];
   const int ntiles = ns * p.nseg[lv];
   const int pair = local / ntiles, tile = local - pair * ntiles;
-  gauss_body<K, TIN, NM, WS, GS_THREADS>(p.lv[lv], tile % ns, tile / ns, pair, ns, p.nseg[lv]);
+  gauss_body<K, TIN, NM, WS, GS_THREADS, false, false>(p.lv[lv], tile % ns, tile / ns, pair, ns, p.nseg[lv]);
 }
 
 template <int K, typename TIN, int NM, int VC = GS_THREADS, bool WS = true>
@@ -669,11 +671,14 @@ int launch_ws(const GaussArgs& a, dim3 grid, cudaStream_t st) {
 
 template <int K, typename TIN, int NM>
 int launch_nm(const GaussArgs& a, dim3 grid, cudaStream_t st) {
+  // map outputs only from the classic kernel (the planner keeps such launches at 128 columns)
+  const bool maps = (a.want & (SSK_MAP_TERMS | SSK_MAP_STATS)) != 0;
+  if (maps && a.vcols != GS_THREADS) return SSK_E_ARG;
   if (NM == 4 && a.vcols == 256) {
     if constexpr (sizeof(TIN) <= 2 && 256 - (K - 1) >= 16) return launch_ws<K, TIN, NM, 256>(a, grid, st);
     return SSK_E_ARG;
   }
-  if (NM == 4 && gauss_ws_enabled()) return launch_ws<K, TIN, NM, GS_THREADS>(a, grid, st);
+  if (NM == 4 && !maps && gauss_ws_enabled()) return launch_ws<K, TIN, NM, GS_THREADS>(a, grid, st);
   auto fn = gauss_pair_kernel<K, TIN, NM>;
   const size_t smem = smem_bytes<K, TIN, NM, GS_THREADS, false>();
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
