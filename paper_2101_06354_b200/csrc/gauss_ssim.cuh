@@ -248,7 +248,21 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
   const int wo = a.wo;
   const bool exact_sq = a.exact_sq != 0;
 
-  double tq0 = 0.0, tl0 = 0.0, tc0 = 0.0, tq1 = 0.0, tl1 = 0.0, tc1 = 0.0;
+  // per-thread running sums of q, l, cs over the tile (<= 128 outputs per thread), packed
+  // fp32 pairs (frame f0, f1); widened to fp64 once per tile for the block reduction
+  u64 fq = 0ull, fl = 0ull, fc = 0ull;
+  auto tile_sums = [&](double* v) {
+    float lo, hi;
+    upk(fq, lo, hi);
+    v[0] = lo;
+    v[3] = hi;
+    upk(fl, lo, hi);
+    v[1] = lo;
+    v[4] = hi;
+    upk(fc, lo, hi);
+    v[2] = lo;
+    v[5] = hi;
+  };
   const int htid = WS ? tid - VC : tid;
   const int hg = htid % G, hj = htid / G;  // H item: output row hg of the chunk, columns 8*hj..8*hj+7
 
@@ -378,7 +392,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
       }
       // columns of this item inside the anchor grid (all 8 for interior items at stride 1)
       const int ncol = min(8, wo - ocol0);
-      u64 sq = 0ull, sl = 0ull, scs = 0ull;
+      u64 sq = fq, sl = fl, scs = fc;
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) {
         const u64 m1 = acc[0][jj], m2 = acc[1][jj];
@@ -456,16 +470,9 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
           }
         }
       }
-      float lo, hi;
-      upk(sq, lo, hi);
-      tq0 += lo;
-      tq1 += hi;
-      upk(sl, lo, hi);
-      tl0 += lo;
-      tl1 += hi;
-      upk(scs, lo, hi);
-      tc0 += lo;
-      tc1 += hi;
+      fq = sq;
+      fl = sl;
+      fc = scs;
     }
   };
 
@@ -522,14 +529,15 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
         const int cw = (tid - VC) >> 5;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
           if (t != (int)blockIdx.x) tile_of(t);
-          tq0 = tl0 = tc0 = tq1 = tl1 = tc1 = 0.0;
+          fq = fl = fc = 0ull;
           for (int c = 0; c < nchunks; ++c, ++cc) {
             named_sync(2 + b, 2 * VC);
             hpass(c, vbuf0 + b * VBYTES);
             if (cc + NB < total) named_arrive(2 + NB + b, 2 * VC);
             b = b + 1 == NB ? 0 : b + 1;
           }
-          double v[6] = {tq0, tl0, tc0, tq1, tl1, tc1};
+          double v[6];
+          tile_sums(v);
 #pragma unroll
           for (int i = 0; i < 6; ++i) v[i] = warp_sum(v[i]);
           if ((tid & 31) == 0) {
@@ -580,7 +588,8 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
     }
   }
 
-  double v[6] = {tq0, tl0, tc0, tq1, tl1, tc1};
+  double v[6];
+  tile_sums(v);
 #pragma unroll
   for (int i = 0; i < 6; ++i) v[i] = warp_sum(v[i]);
   if ((tid & 31) == 0) {
