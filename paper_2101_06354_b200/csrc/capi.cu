@@ -136,9 +136,15 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
       const char* e = std::getenv("SSK_WIDE_U16");
       return e ? std::atoi(e) : 0;
     }();
-    const bool wide_ok = p->dtype == SSK_U8 || (p->dtype == SSK_U16 && wide_u16);
+    // coarse pyramid levels (u16 scaled sums): wide strips on the classic multi-level kernel
+    static const int levels_wide = [] {
+      const char* e = std::getenv("SSK_LEVELS_WIDE");  // default on; 0 = 128-column strips
+      return e ? std::atoi(e) : 1;
+    }();
+    const bool coarse_wide = p->dtype == SSK_U16 && p->scale_log2 > 0 && levels_wide;
+    const bool wide_ok = p->dtype == SSK_U8 || (p->dtype == SSK_U16 && (wide_u16 || coarse_wide));
     const bool maps = (want & (SSK_MAP_TERMS | SSK_MAP_STATS)) != 0;  // maps: classic kernel only
-    a.vcols = (gk::gauss_ws_level() >= 1 && wide_ok && !maps && k <= 17 && a.wo >= 480) ? 256 : 128;
+    a.vcols = (gk::gauss_ws_level() >= 1 && wide_ok && !maps && k <= 17 && (a.wo >= 480 || coarse_wide)) ? 256 : 128;
     const int tw = gauss_tw(k, a.vcols);
     const int nstrips = (a.wo + tw - 1) / tw;
     // Segments depend on the frame geometry only (never on the batch size), so a
@@ -524,7 +530,13 @@ int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, const dou
   // 2) SSIM per level: level 0 alone (input type, unless already run fused), the
   //    coarser levels batched
   for (int l = fuse_l1 ? 1 : 0; l < levels;) {
-    if (l == 0 || !plans[l].gauss || plans[l].ga.vcols != GS_THREADS) {  // wide levels launch alone
+    // coarse levels go to the multi-level kernel: 128-column strips, or 256-column strips
+    // for u16 levels planned wide (classic kernel, 2 CTAs/SM); one launch per strip width
+    auto multi = [&](int i) {
+      return i > 0 && plans[i].gauss &&
+             (plans[i].ga.vcols == GS_THREADS || (plans[i].ga.vcols == 256 && plans[i].ga.dtype == SSK_U16));
+    };
+    if (!multi(l)) {  // level 0 and wide u8 / non-Gaussian levels launch alone
       rc = run_plan(plans[l], const_cast<double*>(fa.partials[l]), nullptr, nullptr, st);
       if (rc) return rc;
       ++l;
@@ -534,7 +546,8 @@ int ssk_msssim(const ssk_planes* p, const ssk_window* win, int levels, const dou
     // dispatched before any shorter ones, so the short tiles of the small levels fill
     // the last wave instead of trailing behind it.
     int order[GS_MAX_LEVELS], nl = 0;
-    while (l < levels && nl < GS_MAX_LEVELS && plans[l].gauss && plans[l].ga.vcols == GS_THREADS) order[nl++] = l++;
+    const int vcols = plans[l].ga.vcols;
+    while (l < levels && nl < GS_MAX_LEVELS && multi(l) && plans[l].ga.vcols == vcols) order[nl++] = l++;
     for (int i = 1; i < nl; ++i)
       for (int j = i; j > 0 && plans[order[j]].ga.seg_rows > plans[order[j - 1]].ga.seg_rows; --j)
         std::swap(order[j], order[j - 1]);

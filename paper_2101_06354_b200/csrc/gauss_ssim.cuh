@@ -628,8 +628,8 @@ __global__ void __launch_bounds__(2 * VC, 1)
 // All pyramid levels of one sample type in one launch: blockIdx.x enumerates the
 // (level, segment, strip) tiles, so the small coarse levels share the GPU with
 // each other instead of each launching a few dozen CTAs.
-template <int K, typename TIN, int NM, bool WS>
-__global__ void __launch_bounds__(WS ? 2 * GS_THREADS : GS_THREADS, WS ? 2 : 4)
+template <int K, typename TIN, int NM, bool WS, int VC = GS_THREADS>
+__global__ void __launch_bounds__(WS ? 2 * VC : VC, WS ? 2 : (VC == 256 ? 2 : 4))
     gauss_levels_kernel(const __grid_constant__ GaussLevels p) {
   int lv = 0;
 #pragma unroll
@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(WS ? 2 * GS_THREADS : GS_THREADS, WS ? 2 : 4)
   const int ns = p.nstrips[lv];
   const int ntiles = ns * p.nseg[lv];
   const int pair = local / ntiles, tile = local - pair * ntiles;
-  gauss_body<K, TIN, NM, WS, GS_THREADS, false, false>(p.lv[lv], tile % ns, tile / ns, pair, ns, p.nseg[lv]);
+  gauss_body<K, TIN, NM, WS, VC, false, false>(p.lv[lv], tile % ns, tile / ns, pair, ns, p.nseg[lv]);
 }
 
 template <int K, typename TIN, int NM, int VC = GS_THREADS, bool WS = true>
@@ -707,6 +707,18 @@ template <int K, typename TIN>
 int launch_levels_one(const GaussLevels& p, dim3 grid, cudaStream_t st) {
   // the coarse levels stay on the classic (non-specialised) kernel: measured faster there
   // (small tiles, 3-4 CTAs/SM); SSK_GAUSS_WS=2 forces the warp-specialised variant
+  if constexpr (K <= 17) {
+    if (p.lv[0].vcols == 256) {  // wide strips (240 outputs), 2 CTAs of 256 threads per SM
+      auto fw = gauss_levels_kernel<K, TIN, 4, false, 256>;
+      const size_t smem = smem_bytes<K, TIN, 4, 256, false>();
+      if (cudaFuncSetAttribute(fw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return SSK_E_CUDA;
+      fw<<<grid, 256, smem, st>>>(p);
+      note_launch();
+      return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+    }
+  }
+  if (p.lv[0].vcols != GS_THREADS) return SSK_E_ARG;
   const bool ws = gauss_ws_level() >= 2;
   auto fn = ws ? gauss_levels_kernel<K, TIN, 4, true> : gauss_levels_kernel<K, TIN, 4, false>;
   const size_t smem = ws ? smem_bytes<K, TIN, 4>() + (size_t)(GS_NBUF - 1) * 4 * G * vp_of(GS_THREADS)
