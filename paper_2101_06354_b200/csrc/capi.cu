@@ -1,6 +1,7 @@
 // C ABI entry points (include/ssimk.h): argument validation, launch planning,
 // workspace carving and the MS-SSIM level loop.  Host-side C++; no allocation
 // inside the calls (all scratch comes from the caller's workspace).
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -150,7 +151,12 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
     // Segments depend on the frame geometry only (never on the batch size), so a
     // frame's fp32 partial sums -- and hence its score -- are bit-identical
     // however frames are batched or sharded.
-    int nseg = (a.ho + 127) / 128;
+    static const int coarse_seg = [] {  // target rows per segment of the coarse levels
+      const char* e = std::getenv("SSK_LEVEL_SEG");
+      return e ? std::max(16, std::atoi(e)) : 128;
+    }();
+    const int seg_target = (p->scale_log2 > 0) ? coarse_seg : 128;
+    int nseg = (a.ho + seg_target - 1) / seg_target;
     a.seg_rows = (a.ho + nseg - 1) / nseg;
     if (a.vcols == 256) a.seg_rows += a.seg_rows & 1;  // even: segments own whole 2x2 pyramid blocks
     nseg = (a.ho + a.seg_rows - 1) / a.seg_rows;
