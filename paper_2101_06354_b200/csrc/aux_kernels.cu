@@ -434,38 +434,44 @@ int launch_pyramid(const PyramidArgs& p, int src_dtype, int dst_dtype, int nl, i
 // the normalised sum).
 // ---------------------------------------------------------------------------
 __global__ void msssim_finalize_kernel(const __grid_constant__ FinalizeArgs a) {
-  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (f >= a.n) return;
-  double combined = a.aggregation == 2 ? 0.0 : 1.0;
-  for (int l = 0; l < a.levels; ++l) {
+  // one block per frame: warp l folds level l (in parallel, same lane-strided order as a
+  // single warp would), warps levels..levels+2 the level-0 SSIM sums; thread 0 combines
+  // the per-level terms in level order
+  __shared__ double s_term[SSK_MAX_SCALES];
+  const int f = blockIdx.x;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w < a.levels) {
+    const int l = w;
     const double* p = a.partials[l] + (long long)f * a.nparts[l] * 3;
     const int comp = (l == a.levels - 1) ? 0 : 2;
     double s = 0.0;
     for (int i = lane; i < a.nparts[l]; i += 32) s += p[(long long)i * 3 + comp];
     s = warp_sum(s);
-    const double mean = __ddiv_rn(s, a.count[l]);
-    if (l == 0 && a.ssim_sums) {
-      for (int c = 0; c < 3; ++c) {
-        double t = 0.0;
-        for (int i = lane; i < a.nparts[0]; i += 32) t += p[(long long)i * 3 + c];
-        t = warp_sum(t);
-        if (lane == 0) a.ssim_sums[(long long)f * 3 + c] = __ddiv_rn(t, a.count[0]);
-      }
-    }
     if (lane == 0) {
+      const double mean = __ddiv_rn(s, a.count[l]);
       a.level_means[(long long)f * a.levels + l] = mean;
-      if (a.aggregation == 2) combined += a.exps[l] * mean;
-      else combined *= pow(fmax(mean, 0.0), a.exps[l]);
+      s_term[l] = a.aggregation == 2 ? a.exps[l] * mean : pow(fmax(mean, 0.0), a.exps[l]);
     }
+  } else if (a.ssim_sums && w < a.levels + 3) {
+    const int c = w - a.levels;
+    const double* p = a.partials[0] + (long long)f * a.nparts[0] * 3;
+    double t = 0.0;
+    for (int i = lane; i < a.nparts[0]; i += 32) t += p[(long long)i * 3 + c];
+    t = warp_sum(t);
+    if (lane == 0) a.ssim_sums[(long long)f * 3 + c] = __ddiv_rn(t, a.count[0]);
   }
-  if (lane == 0 && a.scores && a.aggregation != 0) a.scores[f] = combined;
+  __syncthreads();
+  if (threadIdx.x == 0 && a.scores && a.aggregation != 0) {
+    double combined = a.aggregation == 2 ? 0.0 : 1.0;
+    for (int l = 0; l < a.levels; ++l) combined = a.aggregation == 2 ? combined + s_term[l] : combined * s_term[l];
+    a.scores[f] = combined;
+  }
 }
 
 int launch_msssim_finalize(const FinalizeArgs& a, cudaStream_t st) {
-  const int threads = 256;
-  const int blocks = (a.n * 32 + threads - 1) / threads;
-  msssim_finalize_kernel<<<blocks, threads, 0, st>>>(a);
+  if (a.n < 1) return SSK_OK;
+  if (a.levels < 1 || a.levels > SSK_MAX_SCALES) return SSK_E_ARG;
+  msssim_finalize_kernel<<<a.n, 32 * (a.levels + 3), 0, st>>>(a);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
 }
