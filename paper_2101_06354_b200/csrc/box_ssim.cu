@@ -150,6 +150,28 @@ __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_consta
   double sq = 0.0, sl = 0.0, scs = 0.0, sq2 = 0.0;
   issue_stage(0, 0);
 
+  // MOM with chunks of <= MCH rows: the chunk's 5 x CH moment values of this column are
+  // loaded into registers one chunk ahead (issued before the previous chunk's horizontal
+  // pass), so HBM latency overlaps compute instead of stalling every row
+  constexpr int MCH = 8;
+  const bool mom_pre = MOM && CH <= MCH;
+  long long mv[MOM ? MCH : 1][5];
+  auto load_moments = [&](int chunk) {
+    if constexpr (MOM) {
+      const int colx = c0 + tid;
+      const int rb = r0 + chunk * CH;
+#pragma unroll
+      for (int g = 0; g < MCH; ++g) {
+        const int row = rb + g;
+        const bool ok = g < CH && row < rend && colx < a.w;
+        const long long* mp = a.mom + (long long)(ok ? row : r0) * a.mom_rp + (ok ? colx : 0);
+#pragma unroll
+        for (int m = 0; m < 5; ++m) mv[g][m] = ok ? mp[m * a.mom_plane] : 0ll;
+      }
+    }
+  };
+  if (mom_pre) load_moments(0);
+
   for (int c = 0; c < nchunks; ++c) {
     if (c + 1 < nchunks) {
       issue_stage(c + 1, (c + 1) & 1);
@@ -166,23 +188,7 @@ __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_consta
     const unsigned char* sy = stage + ((c & 1) * 2 + 1) * CH * P + tid * esz;
     const int bfirst = bnext;
     int nemit = 0;
-    for (int g = 0; g < urows; ++g) {
-      if constexpr (MOM) {
-        const int row = r0 + ubase + g, colx = c0 + tid;
-        if (colx < a.w) {
-          const long long* mp = a.mom + (long long)row * a.mom_rp + colx;
-#pragma unroll
-          for (int m = 0; m < 5; ++m) pre[m] += (ACC)mp[m * a.mom_plane];
-        }
-      } else {
-        const ACC x = (ACC)load_sample<TIN>(sx + g * P);
-        const ACC y = (ACC)load_sample<TIN>(sy + g * P);
-        pre[0] += x;
-        pre[1] += y;
-        pre[2] += x * x;
-        pre[3] += y * y;
-        pre[4] += x * y;
-      }
+    auto row_step = [&](const int g) {
       const int u1 = ubase + g + 1;
       if (u1 == emit_at) {
         ACC* vr = vrow + (size_t)nemit * 5 * VP + tid;
@@ -201,6 +207,36 @@ __global__ void __launch_bounds__(BX_THREADS) box_int_kernel(const __grid_consta
         rec_at += s;
         rec_slot = rec_slot + 1 == NSL ? 0 : rec_slot + 1;
       }
+    };
+    if (mom_pre) {
+#pragma unroll
+      for (int g = 0; g < MCH; ++g) {
+        if (g < urows) {
+#pragma unroll
+          for (int m = 0; m < 5; ++m) pre[m] += (ACC)mv[g][m];
+          row_step(g);
+        }
+      }
+      if (c + 1 < nchunks) load_moments(c + 1);
+    }
+    for (int g = 0; g < (mom_pre ? 0 : urows); ++g) {
+      if constexpr (MOM) {
+        const int row = r0 + ubase + g, colx = c0 + tid;
+        if (colx < a.w) {
+          const long long* mp = a.mom + (long long)row * a.mom_rp + colx;
+#pragma unroll
+          for (int m = 0; m < 5; ++m) pre[m] += (ACC)mp[m * a.mom_plane];
+        }
+      } else {
+        const ACC x = (ACC)load_sample<TIN>(sx + g * P);
+        const ACC y = (ACC)load_sample<TIN>(sy + g * P);
+        pre[0] += x;
+        pre[1] += y;
+        pre[2] += x * x;
+        pre[3] += y * y;
+        pre[4] += x * y;
+      }
+      row_step(g);
     }
     __syncthreads();
 

@@ -622,7 +622,11 @@ int plan_volume(const ssk_volume* v, const ssk_window* win, int want, Plan& pl) 
     a.ch = vr * s;
     a.in_pitch = 16;  // no staging for moment planes
     a.nslot = (k + s - 1) / s + 1;
-    int seg_anchors = (256 + s - 1) / s;
+    // a volume is scored one frame at a time: cut the frame into enough segments for
+    // ~4 CTAs per SM of a B200 (592 CTAs; a constant, so results depend on the geometry
+    // only), between 16 and 256 rows per segment
+    const int lo = std::max(1, (16 + s - 1) / s), hi = (256 + s - 1) / s;
+    int seg_anchors = (int)std::min<long long>(hi, std::max<long long>(lo, (pl.gh * (long long)nstrips + 591) / 592));
     long long nseg = (pl.gh + seg_anchors - 1) / seg_anchors;
     seg_anchors = (int)((pl.gh + nseg - 1) / nseg);
     a.seg_anchors = seg_anchors;
