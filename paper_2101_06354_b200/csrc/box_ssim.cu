@@ -360,7 +360,8 @@ static int launch_int_t(const BoxArgs& a, dim3 grid, size_t smem, cudaStream_t s
 }
 
 int launch_box_moments(const BoxArgs& a, dim3 grid, cudaStream_t st) {
-  auto fn = box_int_kernel<uint8_t, unsigned long long, true>;
+  const bool fast = !(a.want & (SSK_MAP_TERMS | SSK_MAP_STATS)) && !a.wsums && a.fast_ok;
+  auto fn = fast ? box_int_kernel<uint8_t, unsigned long long, true, true> : box_int_kernel<uint8_t, unsigned long long, true>;
   const size_t smem = box_smem_bytes(a, true);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return SSK_E_CUDA;

@@ -606,6 +606,12 @@ int plan_volume(const ssk_volume* v, const ssk_window* win, int want, Plan& pl) 
   a.inv_area = 1.0 / a.area;
   a.c1 = win->c1;
   a.c2 = win->c2;
+  // integer-domain score epilogue (box_fast_terms) over the exact temporal window sums:
+  // exact while area^2 * max_sample^2 < 2^52 (samples <= 16 bits)
+  a.area_i = (int)(k * k * v->depth);
+  a.c1d = win->c1 * a.area * a.area;
+  a.c2d = win->c2 * a.area * a.area;
+  a.fast_ok = (a.area * a.area * 65535.0 * 65535.0 < 4.0e15) ? 1 : 0;
   a.want = want;
   a.map_plane = (long long)pl.gh * pl.gw;
   a.map_frame = a.map_plane * ((want & SSK_MAP_STATS) ? 5 : 3);
