@@ -65,17 +65,24 @@ class RollingVolume:
         torch = nat.torch_mod()
         dev = nat.require_device()
         dt = np.float64 if self._is_float else (np.uint8 if self._code == nat.U8 else np.uint16)
-        return torch.from_numpy(np.array(a, dtype=dt, copy=True, order="C")).to(dev)
+        src = a if (a.dtype == dt and a.flags.c_contiguous) else np.ascontiguousarray(a, dtype=dt)
+        # staged through a pinned buffer and copied asynchronously on the current stream
+        tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.uint8): torch.uint8,
+               np.dtype(np.uint16): torch.uint16}[src.dtype]
+        host = torch.empty(src.shape, dtype=tdt, pin_memory=True)
+        host.numpy()[...] = src
+        return host.to(dev, non_blocking=True)
 
     def push(self, ref: PlaneLike, dist: PlaneLike) -> "RollingVolume":
         """Advance the temporal window by one frame pair (src/spatiotemporal.py:60-97)."""
         torch = nat.torch_mod()
         ref, dist = validate_frame_pair(ref, dist)
         a, b = plane_data(ref), plane_data(dist)
+        u8 = a.dtype == np.uint8 and b.dtype == np.uint8  # in range by type: no sample scans
         if self._dims is None:
             self._dims = a.shape
-            ints = a.dtype.kind in "ui" and b.dtype.kind in "ui" and min(a.min(), b.min()) >= 0
-            hi = max(int(a.max()), int(b.max())) if ints else 0
+            ints = u8 or (a.dtype.kind in "ui" and b.dtype.kind in "ui" and min(a.min(), b.min()) >= 0)
+            hi = 255 if u8 else (max(int(a.max()), int(b.max())) if ints else 0)
             self._is_float = not (ints and hi <= 0xFFFF)
             small = a.dtype == np.uint8 and b.dtype == np.uint8
             self._code = nat.F64 if self._is_float else (nat.U8 if small else nat.U16)
@@ -84,7 +91,7 @@ class RollingVolume:
             self._planes = torch.zeros((5, h, w), dtype=dt, device=nat.require_device())
         elif a.shape != self._dims:
             raise DimensionMismatch(f"frame {a.shape[::-1]} pushed into a {self._dims[::-1]} volume")
-        else:
+        elif not (u8 and not self._is_float):
             if not self._is_float:
                 ints = a.dtype.kind in "ui" and b.dtype.kind in "ui"
                 hi = max(int(a.max()), int(b.max())) if ints else 1 << 20
@@ -179,10 +186,15 @@ class RollingVolume:
         return LocalStatsMaps(mu1=m[0], mu2=m[1], var1=m[2], var2=m[3], cov=m[4], window_size=window.k,
                               stride=window.stride, source_dims=self._dims)
 
+    def terms_device(self, window: WindowSpec, config: SsimConfig):
+        """(mean q, mean l, mean cs) of the current 3-D SSIM map as a [3] float64 device tensor
+        (no synchronisation: a series reads all frames' terms back at once)."""
+        sums, _, (gh, gw) = self._run(window, config.c1, config.c2, nat.WANT_Q | nat.WANT_L | nat.WANT_CS)
+        return engine.frame_means(sums, gh * gw)[0]
+
     def terms(self, window: WindowSpec, config: SsimConfig) -> tuple[float, float, float]:
         """(mean q, mean l, mean cs) of the current 3-D SSIM map, fused (no map leaves the GPU)."""
-        sums, _, (gh, gw) = self._run(window, config.c1, config.c2, nat.WANT_Q | nat.WANT_L | nat.WANT_CS)
-        s = engine.frame_means(sums, gh * gw)[0].cpu().numpy()
+        s = self.terms_device(window, config).cpu().numpy()
         return float(s[0]), float(s[1]), float(s[2])
 
 
@@ -201,13 +213,16 @@ def ssim3d_map(vol: RollingVolume, window: WindowSpec, config: SsimConfig = Ssim
 def ssim3d_series(ref_frames: Iterable[PlaneLike], dist_frames: Iterable[PlaneLike], kt: int,
                   config: SsimConfig = SsimConfig()) -> ScoreSeries:
     """Per-frame mean 3-D SSIM of two aligned streams (src/spatiotemporal.py:159-171)."""
+    torch = nat.torch_mod()
     vol = RollingVolume(kt)
-    scores = []
+    terms = []
     for ref, dist in zip(ref_frames, dist_frames):
         validate_frame_pair(ref, dist)
         vol.push(ref, dist)
-        scores.append(vol.terms(config.window, config)[0])
-    return ScoreSeries(np.asarray(scores))
+        terms.append(vol.terms_device(config.window, config))  # read back once, after the last frame
+    if not terms:
+        return ScoreSeries(np.asarray([], dtype=np.float64))
+    return ScoreSeries(torch.stack(terms)[:, 0].cpu().numpy())
 
 
 def shard_with_halo(n_frames: int, rank: int, world: int, kt: int) -> tuple[int, int, int]:
