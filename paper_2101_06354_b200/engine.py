@@ -10,6 +10,7 @@ already satisfies the kernels' alignment contract.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -189,8 +190,11 @@ def _side_streams(device, count: int):
     torch = nat.torch_mod()
     key = device.index
     have = _SIDE_STREAMS.get(key, [])
+    prio = int(os.environ.get("SSK_SIDE_PRIORITY", "1"))
     while len(have) < count:
-        have.append(torch.cuda.Stream(device=device))
+        # optionally the first half's stream at high priority: its coarse levels get CTA
+        # slots ahead of the second half's level-0 tiles as SMs free up
+        have.append(torch.cuda.Stream(device=device, priority=-1 if (prio and not have) else 0))
     _SIDE_STREAMS[key] = have
     return have[:count]
 
