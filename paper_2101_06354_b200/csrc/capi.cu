@@ -155,7 +155,11 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
       const char* e = std::getenv("SSK_LEVEL_SEG");
       return e ? std::max(16, std::atoi(e)) : 128;
     }();
-    const int seg_target = (p->scale_log2 > 0) ? coarse_seg : 128;
+    static const int base_seg = [] {  // target rows per segment of full-resolution frames
+      const char* e = std::getenv("SSK_BASE_SEG");
+      return e ? std::max(16, std::atoi(e)) : 128;
+    }();
+    const int seg_target = (p->scale_log2 > 0) ? coarse_seg : base_seg;
     int nseg = (a.ho + seg_target - 1) / seg_target;
     a.seg_rows = (a.ho + nseg - 1) / nseg;
     if (a.vcols == 256) a.seg_rows += a.seg_rows & 1;  // even: segments own whole 2x2 pyramid blocks
