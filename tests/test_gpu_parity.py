@@ -236,6 +236,25 @@ def test_batch_matches_per_pair(cuda, rng):
     assert np.array_equal(P.ssim_batch(ta, tb, cfg).cpu().numpy(), got)
 
 
+def test_persistent_wide_kernel_multi_tile_ctas(cuda, rng):
+    """41 wide u8 frames = 252 tiles > one CTA per SM: persistent CTAs walk several tiles
+    (the V-tile ring and its barriers continue across tiles) and every frame's score is
+    bit-identical to scoring that frame alone (a handful of tiles, one per CTA)."""
+    import torch
+
+    n, h, w = 41, 512, 600
+    a = rng.integers(0, 256, (n, h, w)).astype(np.uint8)
+    b = np.clip(a.astype(int) + rng.integers(-30, 31, a.shape), 0, 255).astype(np.uint8)
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    terms = P.ssim_terms_batch(ta, tb, cfg)
+    got = torch.stack([terms.score, terms.l_mean, terms.cs_mean], 1).cpu().numpy()
+    for i in (0, 1, 20, 39, 40):
+        one = P.ssim_terms_batch(ta[i:i + 1], tb[i:i + 1], cfg)
+        assert np.array_equal(got[i], np.array([one.score.item(), one.l_mean.item(), one.cs_mean.item()]))
+    assert abs(got[40, 0] - P.ssim_score(a[40], b[40], cfg)) == 0.0
+
+
 @pytest.mark.parametrize("n", [2, 7, 40])
 def test_msssim_side_stream_split_is_bit_identical(cuda, rng, n):
     """Large batches run as sub-batches on side streams (engine.SPLIT_MIN_FRAMES); every
