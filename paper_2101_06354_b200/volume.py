@@ -46,6 +46,7 @@ class RollingVolume:
         self._code: Optional[int] = None
         self._dims: Optional[tuple[int, int]] = None
         self._pushes = 0
+        self._copy_stream = None
 
     @property
     def depth(self) -> int:
@@ -73,7 +74,7 @@ class RollingVolume:
         host.numpy()[...] = src
         return host.to(dev, non_blocking=True)
 
-    def push(self, ref: PlaneLike, dist: PlaneLike) -> "RollingVolume":
+    def push(self, ref: PlaneLike, dist: PlaneLike, staged=None) -> "RollingVolume":
         """Advance the temporal window by one frame pair (src/spatiotemporal.py:60-97)."""
         torch = nat.torch_mod()
         ref, dist = validate_frame_pair(ref, dist)
@@ -97,7 +98,21 @@ class RollingVolume:
                 hi = max(int(a.max()), int(b.max())) if ints else 1 << 20
                 if not ints or min(a.min(), b.min()) < 0 or hi > (255 if self._code == nat.U8 else 0xFFFF):
                     raise ValidationError("frames of one volume must keep the sample type of the first frame")
-        ra, rb = self._upload(a), self._upload(b)
+        if staged is not None and not self._is_float and staged[0].dtype == (
+                torch.uint8 if self._code == nat.U8 else torch.uint16):
+            # pre-staged pinned copies (ssim3d_series' prefetch pool): DMA on a side copy
+            # stream so the upload of this frame overlaps the previous frame's kernels
+            dev = nat.require_device()
+            if self._copy_stream is None:
+                self._copy_stream = torch.cuda.Stream(device=dev)
+            cur = torch.cuda.current_stream(dev)
+            with torch.cuda.stream(self._copy_stream):  # destination allocated on the copy stream
+                ra, rb = staged[0].to(dev, non_blocking=True), staged[1].to(dev, non_blocking=True)
+            cur.wait_stream(self._copy_stream)  # the kernels on `cur` see the frame
+            ra.record_stream(cur)  # freed blocks are reused only after `cur` is done with them
+            rb.record_stream(cur)
+        else:
+            ra, rb = self._upload(a), self._upload(b)
         lib = nat.lib()
         vol = self._volume()
         if self.depth == 0 or self.kt == 1:
@@ -216,10 +231,40 @@ def ssim3d_series(ref_frames: Iterable[PlaneLike], dist_frames: Iterable[PlaneLi
     torch = nat.torch_mod()
     vol = RollingVolume(kt)
     terms = []
-    for ref, dist in zip(ref_frames, dist_frames):
-        validate_frame_pair(ref, dist)
-        vol.push(ref, dist)
-        terms.append(vol.terms_device(config.window, config))  # read back once, after the last frame
+
+    def stage(pair):  # worker thread: copy a u8 / u16 frame pair into pinned host memory
+        out = []
+        for p in pair:
+            a = plane_data(p)
+            if a.dtype not in (np.uint8, np.uint16):
+                return None
+            t = torch.empty(a.shape, dtype=torch.uint8 if a.dtype == np.uint8 else torch.uint16, pin_memory=True)
+            t.numpy()[...] = a
+            out.append(t)
+        return tuple(out)
+
+    # integer frames are staged into pinned memory a few frames ahead on a small thread pool
+    # (numpy copies release the GIL), so uploads are asynchronous DMA and the host loop only
+    # issues launches; scores are read back once, after the last frame
+    from concurrent.futures import ThreadPoolExecutor
+
+    pairs = iter(zip(ref_frames, dist_frames))
+    ahead = deque()
+    with ThreadPoolExecutor(4) as ex:
+        def fill():
+            while len(ahead) < 8:
+                nxt = next(pairs, None)
+                if nxt is None:
+                    return
+                ahead.append((nxt, ex.submit(stage, nxt)))
+
+        fill()
+        while ahead:
+            (ref, dist), fut = ahead.popleft()
+            fill()
+            validate_frame_pair(ref, dist)
+            vol.push(ref, dist, staged=fut.result())
+            terms.append(vol.terms_device(config.window, config))
     if not terms:
         return ScoreSeries(np.asarray([], dtype=np.float64))
     return ScoreSeries(torch.stack(terms)[:, 0].cpu().numpy())
