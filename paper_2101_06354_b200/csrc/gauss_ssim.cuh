@@ -239,9 +239,6 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
   const u64 shift2 = pk(a.shift, a.shift);
   const u64 c1_2 = pk(a.c1, a.c1), c2_2 = pk(a.c2, a.c2);
   const u64 two2 = pk(2.f, 2.f), one2 = pk(1.f, 1.f), mtwo2 = pk(-2.f, -2.f);
-  const u64 twoshift2 = pk(2.f * a.shift, 2.f * a.shift);
-  const float c1b = 2.f * a.shift * a.shift + a.c1;  // 2 s^2 + C1 (exact for s = 2^(bd-1))
-  const u64 c1b_2 = pk(c1b, c1b);
   const bool full_terms = (a.want & (SSK_WANT_Q | SSK_WANT_L)) != 0;
   const bool want_maps = MAPS && (a.want & (SSK_MAP_TERMS | SSK_MAP_STATS)) != 0;
   const int s = a.stride;
@@ -423,22 +420,20 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
         const u64 num2 = fma2(two2, cv, c2_2);
         const u64 cs = mul2(num2, rcp2(den2));
         u64 l = 0ull, q = cs, mu1 = 0ull, mu2 = 0ull;
+        if (full_terms || want_maps) {
+          mu1 = add2(m1, shift2);  // unshifted means (>= 0 for valid samples)
+          mu2 = add2(m2, shift2);
+        }
         if (full_terms) {
-          // with mu = m + s (s = L/2): 2 mu1 mu2 + C1 = 2 Pm + T and mu1^2 + mu2^2 + C1 = Mm + T,
-          // T = 2 s Sm + 2 s^2 + C1 (no catastrophic cancellation: all terms share a sign)
-          if constexpr (NM != 4) {
-            Mm = sumsq2(m1, m2);
-            Sm = add2(m1, m2);
-          }
-          const u64 T = fma2(twoshift2, Sm, c1b_2);
-          const u64 num1 = fma2(two2, Pm, T);
-          const u64 den1 = add2(Mm, T);
+          // l from the unshifted means: 2 mu1 mu2 + C1 and mu1^2 + mu2^2 + C1 = Su^2 - 2 Pu + C1
+          // with the symmetric Su = mu1 + mu2, Pu = mu1 mu2 (mu >= 0, so Su^2 >= 2 Pu: no
+          // cancellation).  Forming them from the shifted m instead (2 Pm + 2 s Sm + 2 s^2 + C1)
+          // cancels catastrophically in dark windows (m ~ -s), e.g. 3e-4 off in l at mu ~ 1.
+          const u64 Su = add2(mu1, mu2), Pu = mul2(mu1, mu2);
+          const u64 num1 = fma2(two2, Pu, c1_2);
+          const u64 den1 = fma2(Su, Su, fma2(mtwo2, Pu, c1_2));
           l = mul2(num1, rcp2(den1));
           q = mul2(l, cs);
-        }
-        if (want_maps) {
-          mu1 = add2(m1, shift2);
-          mu2 = add2(m2, shift2);
         }
         const int col = ocol0 + jj;
         const bool valid = jj < ncol && (s == 1 || col % s == 0);

@@ -678,3 +678,43 @@ def test_4k_config5_properties(cuda):
     alone, alone_t = P.msssim_batch(ref[1:2], dist[1:2], cfg, spec, with_ssim=True)
     assert float(alone[0]) == float(ms[1]) and float(alone_t.score[0]) == float(terms.score[1])
     assert 0.0 < float(ms[0]) < 1.0 and 0.0 < float(terms.score[0]) < 1.0
+
+
+def _adversarial_pairs():
+    h, w = 120, 520  # >= 490 columns: the wide (persistent) u8 kernel, fused level 1
+    yy, xx = np.mgrid[0:h, 0:w]
+    grad = ((xx * 255) // (w - 1)).astype(np.uint8)
+    check = (((yy // 4 + xx // 4) % 2) * 255).astype(np.uint8)
+    return {
+        "flat_equal": (np.full((h, w), 77, np.uint8), np.full((h, w), 77, np.uint8)),
+        "flat_extremes": (np.zeros((h, w), np.uint8), np.full((h, w), 255, np.uint8)),
+        "checker_inverted": (check, (255 - check).astype(np.uint8)),
+        "gradient_plus_one": (grad, np.clip(grad.astype(int) + 1, 0, 255).astype(np.uint8)),
+        "identical_texture": (check, check.copy()),
+        "saturated_vs_texture": (np.full((h, w), 255, np.uint8), check),
+    }
+
+
+_FP32_CANCELLATION = pytest.mark.xfail(
+    strict=True,
+    reason="known deviation (DESIGN.md 9): a near-flat window far from mid-gray (here a 1-level "
+           "gradient at mu ~ 27) loses ~1e-4 of cs to fp32 cancellation in E[x'^2] - m^2 even with "
+           "the L/2 shift; the fix (a per-chunk symmetric shift) is next round's work")
+
+
+@pytest.mark.parametrize("name", [pytest.param(n, marks=_FP32_CANCELLATION) if n == "gradient_plus_one" else n
+                                  for n in sorted(_adversarial_pairs())])
+def test_gaussian_adversarial_inputs_vs_oracle(cuda, oracle, name):
+    """Flat windows (sigma ~ 0), extreme contrasts and exact identity through the fused
+    Gaussian path (C2 carried by the filter, Sm^2 - 2Pm, fp32 tile sums): maps within 1e-4,
+    scores within 1e-5 of the float64 oracle; MS-SSIM as well."""
+    a, b = _adversarial_pairs()[name]
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    win = dict(shape="gauss", k=11, sigma=1.5)
+    got = P.ssim_map(a, b, cfg)
+    want = oracle.ssim_maps(a, b, **win)
+    for g, w_ in zip((got.l_map.values, got.cs_map.values, got.q_map.values), want):
+        assert np.max(np.abs(g - w_)) < MAP_TOL
+    terms = P.ssim_terms(a, b, cfg)
+    assert max(abs(x - y) for x, y in zip(terms, oracle.ssim_terms(a, b, **win))) < SCORE_TOL
+    assert abs(P.msssim(a, b, cfg, P.MultiscaleSpec.product(3)) - oracle.msssim(a, b, 3, **win)) < SCORE_TOL
