@@ -238,7 +238,8 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
   const u64 bias2 = pk(a.conv_bias, a.conv_bias);
   const u64 shift2 = pk(a.shift, a.shift);
   const u64 c1_2 = pk(a.c1, a.c1), c2_2 = pk(a.c2, a.c2);
-  const u64 two2 = pk(2.f, 2.f), one2 = pk(1.f, 1.f), mtwo2 = pk(-2.f, -2.f);
+  const u64 two2 = pk(2.f, 2.f), one2 = pk(1.f, 1.f), half2 = pk(0.5f, 0.5f), mhalf2 = pk(-0.5f, -0.5f);
+  const u64 twoshift2 = pk(2.f * a.shift, 2.f * a.shift);
   const bool full_terms = (a.want & (SSK_WANT_Q | SSK_WANT_L)) != 0;
   const bool want_maps = MAPS && (a.want & (SSK_MAP_TERMS | SSK_MAP_STATS)) != 0;
   const int s = a.stride;
@@ -393,23 +394,21 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) {
         const u64 m1 = acc[0][jj], m2 = acc[1][jj];
-        // Everything below is symmetric in (ref, dist): Pm = m1 m2, Sm = m1 + m2 and
-        // Mm = m1^2 + m2^2 (IEEE scalar ops) are, and every further step uses only them.
-        const u64 Pm = mul2(m1, m2);
-        // exact negation by flipping the sign bits (ALU pipe, not an FMA-pipe subtract);
-        // cov = fma(m1, -m2, E[xy]) stays one rounding
+        // Everything below is symmetric in (ref, dist): it uses only Sm = m1 + m2,
+        // Dq = (m1 - m2)^2 and the exact product inside fma(m1, -m2, E[xy]).
+        // exact negation by flipping the sign bits (ALU pipe, not an FMA-pipe subtract)
         const u64 nm2 = m2 ^ 0x8000000080000000ull;
-        u64 v1, v2, cv, den2, Mm = 0ull, Sm = 0ull;
+        const u64 Sm = add2(m1, m2);
+        const u64 Dm = add2(m1, nm2);  // m1 - m2 (antisymmetric; its square is symmetric)
+        const u64 Dq = mul2(Dm, Dm);
+        u64 v1, v2, cv, den2;
         if constexpr (NM == 4) {
-          // sigma1^2 + sigma2^2 = E[x^2 + y^2] - (m1^2 + m2^2), clamped as a sum:
-          // den2 = max(E[x^2 + y^2] + C2 - Mm, C2) with C2 carried by the filter
-          // m1^2 + m2^2 = Sm^2 - 2 m1 m2 from the symmetric Sm = m1 + m2 and Pm (one FMUL2 +
-          // one FFMA2 instead of six scalar ops; same error order as rounding m1^2 and m2^2)
-          Sm = add2(m1, m2);
-          Mm = fma2(Sm, Sm, mul2(Pm, mtwo2));
-          v1 = maxc_2(sub2(acc[2][jj], Mm), a.c2);
+          // sigma1^2 + sigma2^2 = E[x^2 + y^2] - (m1^2 + m2^2), clamped as a sum, with
+          // 2 (m1^2 + m2^2) = Sm^2 + Dq (no cancellation) and C2 carried by the filter:
+          // den2 = max(E[x^2 + y^2] + C2 - (Sm^2 + Dq) / 2, C2)
+          v1 = maxc_2(fma2(fma2(Sm, Sm, Dq), mhalf2, acc[2][jj]), a.c2);
           v2 = 0ull;
-          cv = fma2(m1, nm2, acc[3][jj]);
+          cv = fma2(m1, nm2, acc[3][jj]);  // cov = E[xy] - m1 m2, one rounding
           den2 = v1;
         } else {
           v1 = max0_2(sub2(acc[2][jj], mul2(m1, m1)));
@@ -420,20 +419,21 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
         const u64 num2 = fma2(two2, cv, c2_2);
         const u64 cs = mul2(num2, rcp2(den2));
         u64 l = 0ull, q = cs, mu1 = 0ull, mu2 = 0ull;
-        if (full_terms || want_maps) {
-          mu1 = add2(m1, shift2);  // unshifted means (>= 0 for valid samples)
-          mu2 = add2(m2, shift2);
-        }
         if (full_terms) {
-          // l from the unshifted means: 2 mu1 mu2 + C1 and mu1^2 + mu2^2 + C1 = Su^2 - 2 Pu + C1
-          // with the symmetric Su = mu1 + mu2, Pu = mu1 mu2 (mu >= 0, so Su^2 >= 2 Pu: no
-          // cancellation).  Forming them from the shifted m instead (2 Pm + 2 s Sm + 2 s^2 + C1)
-          // cancels catastrophically in dark windows (m ~ -s), e.g. 3e-4 off in l at mu ~ 1.
-          const u64 Su = add2(mu1, mu2), Pu = mul2(mu1, mu2);
-          const u64 num1 = fma2(two2, Pu, c1_2);
-          const u64 den1 = fma2(Su, Su, fma2(mtwo2, Pu, c1_2));
+          // l from the unshifted means mu = m + s: with Su = mu1 + mu2 = Sm + 2s,
+          // 2 mu1 mu2 + C1 = (Su^2 - Dq) / 2 + C1 and mu1^2 + mu2^2 + C1 = (Su^2 + Dq) / 2 + C1
+          // (all terms >= 0: no cancellation).  The shifted form 2 Pm + 2 s Sm + 2 s^2 + C1
+          // cancelled catastrophically in dark windows (m ~ -s): 3e-4 off in l at mu ~ 1.
+          const u64 Su = add2(Sm, twoshift2);
+          const u64 H = fma2(mul2(Su, Su), half2, c1_2);
+          const u64 num1 = fma2(Dq, mhalf2, H);
+          const u64 den1 = fma2(Dq, half2, H);
           l = mul2(num1, rcp2(den1));
           q = mul2(l, cs);
+        }
+        if (want_maps) {
+          mu1 = add2(m1, shift2);
+          mu2 = add2(m2, shift2);
         }
         const int col = ocol0 + jj;
         const bool valid = jj < ncol && (s == 1 || col % s == 0);
