@@ -211,3 +211,37 @@ def test_ssim3d_shard_halo_bounds():
     assert [P.shard_with_halo(10, r, 3, 1) for r in range(3)] == [(0, 0, 4), (4, 4, 7), (7, 7, 10)]
     with pytest.raises(E.ValidationError):
         P.shard_with_halo(10, 0, 2, 0)
+
+
+def test_gaussian_epilogue_algebra_matches_ssim_terms():
+    """The fused Gaussian epilogue (csrc/gauss_ssim.cuh, hpass) forms every term from the
+    symmetric Sm = m1 + m2, Dq = (m1 - m2)^2 and Su = Sm + 2s of the shifted means
+    m = mu - s; in float64 this algebra must reproduce src/ssim.py:34-45 term for term, and
+    in float32 it must not cancel in dark windows (the shifted form 2 Pm + 2 s Sm + 2 s^2 + C1
+    lost ~3e-4 of l at mu ~ 1)."""
+    rng = np.random.default_rng(11)
+    s, c1, c2 = 128.0, 6.5025, 58.5225
+    mu1, mu2 = rng.uniform(0, 255, 1000), rng.uniform(0, 255, 1000)
+    var1, var2 = rng.uniform(0, 500, 1000), rng.uniform(0, 500, 1000)
+    cov = rng.uniform(-1, 1, 1000) * np.sqrt(var1 * var2)
+    m1, m2 = mu1 - s, mu2 - s
+    e_sq = var1 + var2 + m1 * m1 + m2 * m2  # E[x'^2 + y'^2]
+    e_xy = cov + m1 * m2
+    sm, dq = m1 + m2, (m1 - m2) ** 2
+    su = sm + 2 * s
+    den2 = (e_sq + c2) - 0.5 * (sm * sm + dq)
+    num2 = 2 * (e_xy - m1 * m2) + c2
+    h = 0.5 * su * su + c1
+    l_new, cs_new = (h - 0.5 * dq) / (h + 0.5 * dq), num2 / den2
+    l_ref = (2 * mu1 * mu2 + c1) / (mu1 ** 2 + mu2 ** 2 + c1)
+    cs_ref = (2 * cov + c2) / (var1 + var2 + c2)
+    assert np.max(np.abs(l_new - l_ref)) < 1e-12 and np.max(np.abs(cs_new - cs_ref)) < 1e-12
+    # float32 in a dark window (mu ~ 1): the Su / Dq form stays accurate, the shifted one does not
+    f = np.float32
+    a, b = f(1.0) - f(s), f(2.0) - f(s)  # m1, m2
+    sm32, dq32 = f(a + b), f((a - b) * (a - b))
+    su32 = f(sm32 + f(2 * s))
+    h32 = f(f(f(0.5) * f(su32 * su32)) + f(c1))
+    l32 = f(f(h32 - f(0.5) * dq32) / f(h32 + f(0.5) * dq32))
+    l64 = (2 * 1.0 * 2.0 + c1) / (1.0 + 4.0 + c1)
+    assert abs(float(l32) - l64) < 1e-6
