@@ -175,8 +175,9 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
     a.c1 = (float)win->c1;
     a.c2 = (float)win->c2;
     a.want = want;
-    // x' = m * 2^-scale with |m| <= 2^(bd-1+scale): x'^2 is exact in fp32 when m^2 fits 24 bits
-    a.exact_sq = (p->dtype != SSK_F32 && p->bit_depth - 1 + p->scale_log2 <= 12) ? 1 : 0;
+    // x' = m * 2^-scale with |m| <= 2^(bd+scale) (per-tile shift anywhere in [0, L]): x'^2 is
+    // exact in fp32 when m^2 fits 24 bits
+    a.exact_sq = (p->dtype != SSK_F32 && p->bit_depth + p->scale_log2 <= 12) ? 1 : 0;
     std::memcpy(a.taps, win->taps, sizeof(a.taps));
     pl.grid = dim3(nstrips, nseg, (p->n + 1) / 2);  // two frames per CTA (packed fp32 pairs)
     pl.nparts_per_frame = (size_t)nstrips * nseg;

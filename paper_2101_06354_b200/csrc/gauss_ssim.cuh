@@ -240,6 +240,51 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
   const u64 c1_2 = pk(a.c1, a.c1), c2_2 = pk(a.c2, a.c2);
   const u64 two2 = pk(2.f, 2.f), one2 = pk(1.f, 1.f), half2 = pk(0.5f, 0.5f), mhalf2 = pk(-0.5f, -0.5f);
   const u64 twoshift2 = pk(2.f * a.shift, 2.f * a.shift);
+  // Per-tile sample shift (integer inputs): instead of the fixed L/2, every tile shifts its
+  // samples by c = round(mean of (x + y) / 2) over its middle input row, per frame --
+  // symmetric in ref / dist, exact (an integer in stored units), and close to the local
+  // level, so E[x'^2] - m^2 cancels far less in near-flat windows away from mid-gray.
+  // vbias / hshift / h2shift carry the tile's shift into the V pass and the epilogue.
+  constexpr bool TSHIFT = ES <= 2;
+  __shared__ unsigned s_tsum[2 * VC / 32][2];
+  u64 vbias = bias2, hshift = shift2, h2shift = twoshift2;
+  auto tile_shift = [&](const int gt, const int gs, const int wbase, auto&& gsync) {
+    const int r = min(y0 + (y1 - y0) / 2 + K / 2, a.h - 1);
+    unsigned v0 = 0u, v1 = 0u;
+    for (int i = gt; i < TWI && c0 + i < a.w; i += gs) {
+      const long long off = (long long)r * a.row_pitch_b + (long long)(c0 + i) * ES;
+      if constexpr (ES == 1) {
+        v0 += (unsigned)a.ref[fo0 + off] + a.dist[fo0 + off];
+        v1 += (unsigned)a.ref[fo1 + off] + a.dist[fo1 + off];
+      } else {
+        v0 += (unsigned)*reinterpret_cast<const unsigned short*>(a.ref + fo0 + off) +
+              *reinterpret_cast<const unsigned short*>(a.dist + fo0 + off);
+        v1 += (unsigned)*reinterpret_cast<const unsigned short*>(a.ref + fo1 + off) +
+              *reinterpret_cast<const unsigned short*>(a.dist + fo1 + off);
+      }
+    }
+    v0 = __reduce_add_sync(0xffffffffu, v0);
+    v1 = __reduce_add_sync(0xffffffffu, v1);
+    if ((gt & 31) == 0) {
+      s_tsum[wbase + (gt >> 5)][0] = v0;
+      s_tsum[wbase + (gt >> 5)][1] = v1;
+    }
+    gsync();
+    unsigned t0 = 0u, t1 = 0u;
+    for (int wi = 0; wi < gs / 32; ++wi) {
+      t0 += s_tsum[wbase + wi][0];
+      t1 += s_tsum[wbase + wi][1];
+    }
+    gsync();  // the scratch is rewritten by the next tile
+    const unsigned n = (unsigned)max(1, min(TWI, a.w - c0));
+    const float sc = a.conv_scale;                        // 2^-scale_log2 (exact)
+    const float cv0 = (float)((t0 + n) / (2u * n)) * sc;  // value units, exact
+    const float cv1 = (float)((t1 + n) / (2u * n)) * sc;
+    const float base = -8388608.f * sc;                   // the 2^23 splice, in value units
+    vbias = pk(base - cv0, base - cv1);                   // exact: (2^23 + c_stored) * 2^-k
+    hshift = pk(cv0, cv1);
+    h2shift = pk(2.f * cv0, 2.f * cv1);
+  };
   const bool full_terms = (a.want & (SSK_WANT_Q | SSK_WANT_L)) != 0;
   const bool want_maps = MAPS && (a.want & (SSK_MAP_TERMS | SSK_MAP_STATS)) != 0;
   const int s = a.stride;
@@ -281,8 +326,8 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
 #pragma unroll
       for (int u = 0; u < G + K - 1; ++u) {
         const unsigned char* rp = (u < wrap ? pa : pb) + u * 4 * RB;
-        const u64 X = fma2(pk(raw_to_float<TIN>(rp), raw_to_float<TIN>(rp + RB)), scale2, bias2);
-        const u64 Y = fma2(pk(raw_to_float<TIN>(rp + 2 * RB), raw_to_float<TIN>(rp + 3 * RB)), scale2, bias2);
+        const u64 X = fma2(pk(raw_to_float<TIN>(rp), raw_to_float<TIN>(rp + RB)), scale2, vbias);
+        const u64 Y = fma2(pk(raw_to_float<TIN>(rp + 2 * RB), raw_to_float<TIN>(rp + 3 * RB)), scale2, vbias);
         u64 P[NM];
         P[0] = X;
         P[1] = Y;
@@ -424,7 +469,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
           // 2 mu1 mu2 + C1 = (Su^2 - Dq) / 2 + C1 and mu1^2 + mu2^2 + C1 = (Su^2 + Dq) / 2 + C1
           // (all terms >= 0: no cancellation).  The shifted form 2 Pm + 2 s Sm + 2 s^2 + C1
           // cancelled catastrophically in dark windows (m ~ -s): 3e-4 off in l at mu ~ 1.
-          const u64 Su = add2(Sm, twoshift2);
+          const u64 Su = add2(Sm, h2shift);
           const u64 H = fma2(mul2(Su, Su), half2, c1_2);
           const u64 num1 = fma2(Dq, mhalf2, H);
           const u64 den1 = fma2(Dq, half2, H);
@@ -432,8 +477,8 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
           q = mul2(l, cs);
         }
         if (want_maps) {
-          mu1 = add2(m1, shift2);
-          mu2 = add2(m2, shift2);
+          mu1 = add2(m1, hshift);
+          mu2 = add2(m2, hshift);
         }
         const int col = ocol0 + jj;
         const bool valid = jj < ncol && (s == 1 || col % s == 0);
@@ -471,6 +516,9 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
     }
   };
 
+  if constexpr (TSHIFT && (!WS || !PERSIST)) {  // one tile per CTA: the whole block computes it
+    tile_shift(tid, NT, 0, [&] { __syncthreads(); });
+  }
   if constexpr (!WS) {
     for (int c = 0; c < nchunks; ++c) {
       cp_async_wait<0>();
@@ -497,8 +545,11 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
       int b = 0, cc = 0;
       if (tid < VC) {  // producers
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+          // each warpgroup pair derives the tile's shift itself from the same samples
+          // (integer sums: bit-identical in both), so no producer -> consumer hand-off
+          if (t != (int)blockIdx.x) tile_of(t);
+          if constexpr (TSHIFT) tile_shift(tid, VC, 0, [&] { named_sync(1, VC); });
           if (t != (int)blockIdx.x) {
-            tile_of(t);
             stage_rows(y0, y0 + G + K - 1);  // the previous tile's raw rows are no longer read
           }
           for (int c = 0; c < nchunks; ++c, ++cc) {
@@ -524,6 +575,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
         const int cw = (tid - VC) >> 5;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
           if (t != (int)blockIdx.x) tile_of(t);
+          if constexpr (TSHIFT) tile_shift(tid - VC, VC, VC / 32, [&] { named_sync(CB, VC); });
           fq = fl = fc = 0ull;
           for (int c = 0; c < nchunks; ++c, ++cc) {
             named_sync(2 + b, 2 * VC);
