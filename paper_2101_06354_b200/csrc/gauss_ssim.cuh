@@ -19,9 +19,11 @@
 //            (ref/dist x 2 frames) into a ring of 2G+K-1 raw rows, one chunk
 //            ahead of the compute (double buffering), zero fill past the edge.
 //   V pass : thread = input column; converts samples exactly to fp32 (u8/u16
-//            via the 2^23-mantissa splice), subtracts the symmetric shift L/2
-//            (keeps E[x^2]-E[x]^2 well conditioned in fp32 and preserves exact
-//            ref/dist symmetry), forms x, y, x^2, y^2, xy and gathers the
+//            via the 2^23-mantissa splice), subtracts a symmetric shift -- per
+//            tile, the rounded mean of (x + y) / 2 over the tile's middle row
+//            for integer samples, L/2 otherwise (keeps E[x^2]-E[x]^2 well
+//            conditioned in fp32 and preserves exact ref/dist symmetry),
+//            forms x, y, x^2, y^2, xy and gathers the
 //            K-tap vertical filter for G output rows (5*G packed accumulators).
 //   H pass : thread = (output row, 8 adjacent columns); K-tap horizontal filter
 //            from the shared-memory V rows, then the SSIM epilogue on packed
