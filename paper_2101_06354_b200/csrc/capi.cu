@@ -361,9 +361,15 @@ const char* ssk_strerror(int code) {
 }
 
 size_t ssk_ssim_workspace_bytes(const ssk_planes* p, const ssk_window* win) {
-  Plan pl;
-  if (plan_ssim(p, win, SSK_WANT_Q | SSK_WANT_L | SSK_WANT_CS, pl)) return 0;
-  return partial_bytes(pl, p->n) * (pl.gauss ? 1 : 2);  // rect: room for the q^2 partials
+  // enough for any `want`: map launches run on narrower strips (more partials) than
+  // score-only launches, so take the larger of the two plans
+  size_t bytes = 0;
+  for (const int want : {SSK_WANT_Q | SSK_WANT_L | SSK_WANT_CS, SSK_WANT_Q | SSK_MAP_TERMS}) {
+    Plan pl;
+    if (plan_ssim(p, win, want, pl)) return 0;
+    bytes = std::max(bytes, partial_bytes(pl, p->n) * (pl.gauss ? 1 : 2));  // rect: room for q^2
+  }
+  return bytes;
 }
 
 int ssk_ssim(const ssk_planes* p, const ssk_window* win, int want, double* d_sums, void* d_maps,

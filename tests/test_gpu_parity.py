@@ -712,3 +712,38 @@ def test_gaussian_adversarial_inputs_vs_oracle(cuda, oracle, name):
     terms = P.ssim_terms(a, b, cfg)
     assert max(abs(x - y) for x, y in zip(terms, oracle.ssim_terms(a, b, **win))) < SCORE_TOL
     assert abs(P.msssim(a, b, cfg, P.MultiscaleSpec.product(3)) - oracle.msssim(a, b, 3, **win)) < SCORE_TOL
+
+
+@pytest.mark.parametrize("want_maps", [False, True])
+@pytest.mark.parametrize("h,w", [(300, 520), (1080, 1920), (64, 700)])
+def test_workspace_query_covers_every_launch(cuda, h, w, want_maps):
+    """ssk_ssim_workspace_bytes must cover map launches too (they run on narrower strips,
+    i.e. more partials, than score-only launches of the wide u8 kernel): a workspace of
+    exactly the queried size works for both (the cached pool in engine would hide a short
+    query in a long test session)."""
+    import ctypes
+
+    import torch
+    from paper_2101_06354_b200 import _native as nat
+
+    rng = np.random.default_rng(h + w)
+    a = torch.from_numpy(rng.integers(0, 256, (2, h, w)).astype(np.uint8)).cuda()
+    b = torch.from_numpy(rng.integers(0, 256, (2, h, w)).astype(np.uint8)).cuda()
+    pair = engine.device_pair(a, b, 8, gauss=True)
+    window = P.WindowSpec.gaussian(1.5)
+    cfg = P.SsimConfig(window=window)
+    lib = nat.lib()
+    planes, win = pair.planes(), nat.make_window(window, cfg.c1, cfg.c2)
+    size = lib.ssk_ssim_workspace_bytes(ctypes.byref(planes), ctypes.byref(win))
+    ws = torch.empty(size, dtype=torch.uint8, device="cuda")
+    want = nat.WANT_Q | nat.WANT_L | nat.WANT_CS
+    sums = torch.empty((2, 3), dtype=torch.float64, device="cuda")
+    maps = None
+    if want_maps:
+        gh, gw = engine.grid_shape(h, w, 11, 1)
+        maps = torch.empty((2, 3, gh, gw), dtype=torch.float32, device="cuda")
+        want |= nat.MAP_TERMS
+    rc = lib.ssk_ssim(ctypes.byref(planes), ctypes.byref(win), want, sums.data_ptr(),
+                      None if maps is None else maps.data_ptr(), ws.data_ptr(), ws.numel(),
+                      nat.stream_handle(None))
+    assert rc == 0, nat.lib().ssk_strerror(rc)
