@@ -250,6 +250,16 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
   constexpr bool TSHIFT = ES <= 2;
   __shared__ unsigned s_tsum[2 * VC / 32][2];
   u64 vbias = bias2, hshift = shift2, h2shift = twoshift2;
+  auto set_shift = [&](const unsigned t0, const unsigned t1) {  // sums of (x + y) over n columns
+    const unsigned n = (unsigned)max(1, min(TWI, a.w - c0));
+    const float sc = a.conv_scale;                        // 2^-scale_log2 (exact)
+    const float cv0 = (float)((t0 + n) / (2u * n)) * sc;  // value units, exact
+    const float cv1 = (float)((t1 + n) / (2u * n)) * sc;
+    const float base = -8388608.f * sc;                   // the 2^23 splice, in value units
+    vbias = pk(base - cv0, base - cv1);                   // exact: (2^23 + c_stored) * 2^-k
+    hshift = pk(cv0, cv1);
+    h2shift = pk(2.f * cv0, 2.f * cv1);
+  };
   auto tile_shift = [&](const int gt, const int gs, const int wbase, auto&& gsync) {
     const int r = min(y0 + (y1 - y0) / 2 + K / 2, a.h - 1);
     unsigned v0 = 0u, v1 = 0u;
@@ -278,14 +288,40 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
       t1 += s_tsum[wbase + wi][1];
     }
     gsync();  // the scratch is rewritten by the next tile
-    const unsigned n = (unsigned)max(1, min(TWI, a.w - c0));
-    const float sc = a.conv_scale;                        // 2^-scale_log2 (exact)
-    const float cv0 = (float)((t0 + n) / (2u * n)) * sc;  // value units, exact
-    const float cv1 = (float)((t1 + n) / (2u * n)) * sc;
-    const float base = -8388608.f * sc;                   // the 2^23 splice, in value units
-    vbias = pk(base - cv0, base - cv1);                   // exact: (2^23 + c_stored) * 2^-k
-    hshift = pk(cv0, cv1);
-    h2shift = pk(2.f * cv0, 2.f * cv1);
+    set_shift(t0, t1);
+  };
+  // Per-chunk variant for the classic kernel's map launches (same threads run the V and H
+  // passes of a chunk, so nothing is handed over): the shift follows the chunk's own rows,
+  // e.g. both sides of a letterbox edge inside a tile.  Reads the staged middle row.
+  auto chunk_shift_smem = [&](const int c) {
+    const int row = min(y0 + c * G + (G + K - 1) / 2, in_end - 1);
+    const unsigned char* rp = raw + (((row - y0) % RR) * 4) * RB + tid * ES;
+    unsigned v0 = 0u, v1 = 0u;
+    if (tid < TWI && c0 + tid < a.w) {
+      if constexpr (ES == 1) {
+        v0 = (unsigned)rp[0] + rp[2 * RB];
+        v1 = (unsigned)rp[RB] + rp[3 * RB];
+      } else {
+        v0 = (unsigned)*reinterpret_cast<const unsigned short*>(rp) +
+             *reinterpret_cast<const unsigned short*>(rp + 2 * RB);
+        v1 = (unsigned)*reinterpret_cast<const unsigned short*>(rp + RB) +
+             *reinterpret_cast<const unsigned short*>(rp + 3 * RB);
+      }
+    }
+    v0 = __reduce_add_sync(0xffffffffu, v0);
+    v1 = __reduce_add_sync(0xffffffffu, v1);
+    if ((tid & 31) == 0) {
+      s_tsum[tid >> 5][0] = v0;
+      s_tsum[tid >> 5][1] = v1;
+    }
+    __syncthreads();
+    unsigned t0 = 0u, t1 = 0u;
+    for (int wi = 0; wi < NT / 32; ++wi) {
+      t0 += s_tsum[wi][0];
+      t1 += s_tsum[wi][1];
+    }
+    __syncthreads();
+    set_shift(t0, t1);
   };
   const bool full_terms = (a.want & (SSK_WANT_Q | SSK_WANT_L)) != 0;
   const bool want_maps = MAPS && (a.want & (SSK_MAP_TERMS | SSK_MAP_STATS)) != 0;
@@ -525,6 +561,9 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
     for (int c = 0; c < nchunks; ++c) {
       cp_async_wait<0>();
       __syncthreads();  // chunk c's rows landed; the previous H pass is done with the V tile
+      if constexpr (TSHIFT) {
+        if (want_maps) chunk_shift_smem(c);  // uniform branch
+      }
       vpass(c, vbuf0);
       __syncthreads();  // V tile complete; the chunk's G oldest raw rows are free
       if (c + 1 < nchunks) stage_rows(y0 + (c + 1) * G + K - 1, y0 + (c + 2) * G + K - 1);

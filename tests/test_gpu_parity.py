@@ -747,3 +747,23 @@ def test_workspace_query_covers_every_launch(cuda, h, w, want_maps):
                       None if maps is None else maps.data_ptr(), ws.data_ptr(), ws.numel(),
                       nat.stream_handle(None))
     assert rc == 0, nat.lib().ssk_strerror(rc)
+
+
+@pytest.mark.parametrize("bar", [20, 64, 150])
+def test_gaussian_letterbox_bars_vs_oracle(cuda, oracle, bar):
+    """Near-flat dark bars (0-2 noise) above 1/f content: the map launches shift every 8-row
+    chunk by its own rows' level (a bar edge inside a tile no longer cancels in fp32; was up
+    to 3e-4 off in cs with one shift per tile); scores (per-tile shift) within 1e-5."""
+    from paper_2101_06354_b200 import synth
+
+    rng = np.random.default_rng(bar)
+    a = synth.inv_f_noise(rng, 300, 520, 255.0).astype(np.uint8)
+    a[:bar] = rng.integers(0, 3, (bar, 520))
+    b = np.clip(a.astype(int) + rng.integers(-1, 2, a.shape), 0, 255).astype(np.uint8)
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    win = dict(shape="gauss", k=11, sigma=1.5)
+    got = P.ssim_map(a, b, cfg)
+    for g, w_ in zip((got.l_map.values, got.cs_map.values, got.q_map.values), oracle.ssim_maps(a, b, **win)):
+        assert np.max(np.abs(g - w_)) < MAP_TOL
+    terms = P.ssim_terms(a, b, cfg)
+    assert max(abs(x - y) for x, y in zip(terms, oracle.ssim_terms(a, b, **win))) < SCORE_TOL
