@@ -17,9 +17,14 @@ Multi-GPU (torchrun): weak scaling, each rank scores its own 64 frames; no
 collective on the data path; ranks meet only at the barriers around the timed
 region and in one all_reduce(MAX) of the elapsed time.
 
---impl reference: times the reference's CPU algorithm (the oracle port; the
-reference itself is pure Python and cannot be installed on the GPU box) on the
-host cores for the same metric/config; rank 0 only.
+--gpus N without torchrun: bench.py re-launches itself under
+torch.distributed.run with N ranks (one per GPU, 127.0.0.1 rendezvous); each
+rank binds its host threads to its GPU's NUMA node before it pins its frames.
+
+--impl reference: times the reference's own CPU implementation (ssimkit,
+installed untracked under baseline/_ref by tools/install_reference.sh; the
+oracle port when that is absent) on the host cores for the same metric and
+config; rank 0 only.
 """
 
 from __future__ import annotations
@@ -72,25 +77,62 @@ def generate(indices, workers: int):
 # CPU baseline (oracle port; test infrastructure used only as the measured baseline)
 # ---------------------------------------------------------------------------
 
-def _cpu_score(pair) -> float:
-    """One frame pair through the reference's CPU algorithm (oracle port): ssim_score + msssim."""
+REF_DIR = REPO / "baseline" / "_ref"
+
+
+def _reference_impl():
+    """The reference package itself (pure Python ssimkit under baseline/_ref) when it is
+    installed, else the oracle port of its numpy algorithms.  Returns (kind, score_fn)."""
+    if (REF_DIR / "ssimkit" / "__init__.py").exists():
+        if str(REF_DIR) not in sys.path:
+            sys.path.insert(0, str(REF_DIR))
+        import ssimkit
+        from ssimkit.config import MultiscaleSpec, SsimConfig, WindowSpec
+
+        cfg = SsimConfig(window=WindowSpec.gaussian(SIGMA, k=K))
+        spec = MultiscaleSpec.product(LEVELS)
+
+        def score(a, b):
+            ssimkit.ssim_score(a, b, cfg)       # the reference's public API, stock code path
+            ssimkit.msssim(a, b, cfg, spec)
+            return 1.0
+
+        return "reference", score
     from oracle import ssim_oracle as O
 
-    a, b = pair
     win = dict(shape="gauss", k=K, sigma=SIGMA)
-    O.ssim_terms(a, b, **win)       # ssim_score path (the reference computes it separately)
-    O.msssim(a, b, LEVELS, **win)   # msssim path
-    return 1.0
+
+    def score(a, b):
+        O.ssim_terms(a, b, **win)       # ssim_score path (the reference computes it separately)
+        O.msssim(a, b, LEVELS, **win)   # msssim path
+        return 1.0
+
+    return "port", score
+
+
+_SCORE = None
+
+
+def _cpu_score(pair) -> float:
+    """One frame pair through the reference's CPU path: ssim_score + msssim (Gaussian 11/1.5)."""
+    global _SCORE
+    if _SCORE is None:
+        _SCORE = _reference_impl()[1]
+    return _SCORE(*pair)
 
 
 def _cpu_warm(_) -> int:
-    import oracle.ssim_oracle  # noqa: F401  (imports outside the timed region)
-
+    global _SCORE
+    _SCORE = _reference_impl()[1]  # imports outside the timed region
     return os.getpid()
 
 
+def cpu_kind() -> str:
+    return "reference" if (REF_DIR / "ssimkit" / "__init__.py").exists() else "port"
+
+
 class CpuBaseline:
-    """A persistent pool of single-threaded worker processes running the oracle port.
+    """A persistent pool of single-threaded worker processes running the reference's CPU path.
 
     Inputs are generated up front and worker start-up/imports happen before any timing, so the
     timed region holds only the reference algorithm (plus pickling the 4 MB pair to a worker).
@@ -99,8 +141,7 @@ class CpuBaseline:
     def __init__(self, workers: int):
         from concurrent.futures import ProcessPoolExecutor
 
-        for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
-            os.environ[k] = "1"
+        single_threaded_blas()
         self.workers = workers
         self.pool = ProcessPoolExecutor(workers)
         list(self.pool.map(_cpu_warm, range(workers)))
@@ -115,16 +156,61 @@ class CpuBaseline:
         self.pool.shutdown()
 
 
+def single_threaded_blas() -> None:
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
+
+
+def cpu_context(pairs, cores: int) -> dict:
+    """The two context figures SURVEY.md 8(d) asks for beside the all-process rate: one core
+    (one pair in this process) and the reference's own frame-parallel mechanism, a
+    ThreadPoolExecutor over the frames (src/pipeline.py:319-322), with `cores` threads."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    _cpu_warm(0)
+    t0 = time.perf_counter()
+    _cpu_score(pairs[0])
+    one = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(cores) as ex:
+        done = sum(ex.map(_cpu_score, pairs))
+    tp = time.perf_counter() - t0
+    return {"single_core": {"value": 1.0 / one, "unit": UNIT, "cores": 1, "sample": "1 config-2 pair"},
+            "thread_pool": {"value": done / tp, "unit": UNIT, "cores": cores,
+                            "sample": f"{len(pairs)} config-2 pairs on a {cores}-thread ThreadPoolExecutor "
+                                      "(the reference's frame-parallel mechanism, src/pipeline.py:319-322)"}}
+
+
 def cpu_pairs(n: int, workers: int):
     ref, dist = generate(range(10_000, 10_000 + n), workers)
     return [(ref[i], dist[i]) for i in range(n)]
 
 
 def host_cores() -> int:
+    """Usable host cores: the affinity mask, capped by a cgroup CPU quota if one is set."""
     try:
-        return len(os.sched_getaffinity(0))
+        n = len(os.sched_getaffinity(0))
     except AttributeError:
-        return os.cpu_count() or 1
+        n = os.cpu_count() or 1
+    try:
+        quota, period = Path("/sys/fs/cgroup/cpu.max").read_text().split()[:2]
+        if quota != "max":
+            n = min(n, max(1, int(float(quota) / float(period))))
+    except (OSError, ValueError):
+        pass
+    return n
+
+
+def host_info() -> dict:
+    model = None
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "usable_cores": host_cores()}
 
 
 # ---------------------------------------------------------------------------
@@ -218,16 +304,105 @@ def dist_env():
     return world, rank, local
 
 
+def bench_config(world: int) -> dict:
+    """The workload dict, identical in both arms (the driver compares them)."""
+    return {"workload": WORKLOAD, "batch": BATCH, "h": H, "w": W, "window": "gauss 11/1.5",
+            "levels": LEVELS, "seed_base": 202, "parallelism": f"frame-shard x{world} (weak)",
+            "l2": "inputs 265 MB per step > 126 MB L2 (no flush needed)"}
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch_if_needed(args) -> None:
+    """`bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run with N ranks
+    (one process per GPU).  Under torchrun the world size must equal --gpus."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return
+    if args.gpus <= 1 or args.impl == "reference":
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
+def gpu_numa_cpus(device_index: int):
+    """(numa node, cpu list) of the GPU's PCI device from sysfs, or (None, None)."""
+    import torch
+
+    p = torch.cuda.get_device_properties(device_index)
+    bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+    try:
+        node = int(Path(f"/sys/bus/pci/devices/{bus}/numa_node").read_text())
+    except (OSError, ValueError):
+        return None, None
+    if node < 0:
+        return None, None
+    try:
+        spec = Path(f"/sys/devices/system/node/node{node}/cpulist").read_text().strip()
+    except OSError:
+        return node, None
+    cpus = set()
+    for part in spec.split(","):
+        lo, _, hi = part.partition("-")
+        cpus.update(range(int(lo), int(hi or lo) + 1))
+    return node, sorted(cpus)
+
+
+def bind_numa(device_index: int) -> dict:
+    """Bind this rank's host threads (and so the first touch of its pinned frames) to the
+    CPUs of its GPU's NUMA node."""
+    node, cpus = gpu_numa_cpus(device_index)
+    if not cpus:
+        return {"numa_node": node, "bound": False}
+    try:
+        allowed = os.sched_getaffinity(0)
+        use = [c for c in cpus if c in allowed]
+        if use:
+            os.sched_setaffinity(0, use)
+            return {"numa_node": node, "bound": True, "cpus": len(use)}
+    except (AttributeError, OSError):
+        pass
+    return {"numa_node": node, "bound": False}
+
+
+def launch_selftest(args) -> None:
+    """CPU check of the launcher: every rank joins a gloo group and rank 0 prints who came up."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    dist.init_process_group("gloo")
+    t = torch.tensor([rank, local, os.getpid()], dtype=torch.int64)
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    if rank == 0:
+        print(json.dumps({"n_gpus": world, "ranks": [int(x[0]) for x in out],
+                          "local_ranks": [int(x[1]) for x in out],
+                          "pids": len({int(x[2]) for x in out})}), flush=True)
+    dist.destroy_process_group()
+
+
 def run_reference(args) -> None:
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    single_threaded_blas()
     cores = host_cores()
     per_step = cores  # one pair per worker process per step
     pairs = cpu_pairs(per_step, cores)
     cpu = CpuBaseline(cores)
     # warm-up steps run the same algorithm on 256x512 crops of the step's pairs (worker
-    # imports, allocator and caches warmed; a full 1080p step is ~12 s of CPU per pair)
+    # imports, allocator and caches warmed; a full 1080p step is several s of CPU per pair)
     crops = [(a[:256, :512].copy(), b[:256, :512].copy()) for a, b in pairs]
     for _ in range(args.warmup):
         cpu.rate(crops)
@@ -237,14 +412,21 @@ def run_reference(args) -> None:
         t_total += wall
     cpu.close()
     value = per_step * args.steps / t_total
+    kind = cpu_kind()
+    what = ("the reference package itself (ssimkit from baseline/_ref: ssim_score + msssim per pair)"
+            if kind == "reference" else "oracle port of ssimkit's numpy path (ssim_score + msssim per pair)")
+    cpu_base = {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                "sample": f"{per_step} config-2 pairs per step (1 per single-threaded worker process), {what}",
+                "host": host_info()}
+    if not args.no_cpu_context:
+        cpu_base.update(cpu_context(pairs, cores))
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": max(world, args.gpus),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "batch": BATCH, "h": H, "w": W, "seed_base": 202},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{per_step} config-2 pairs per step (1 per single-threaded worker process), "
-                                   "oracle port of ssimkit's numpy path (ssim_score + msssim per pair)"},
+        "data": "synthetic", "config": bench_config(max(world, args.gpus)),
+        "sample_pairs_per_step": per_step,
+        "cpu_baseline": cpu_base,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -259,10 +441,13 @@ def run_b200(args) -> None:
     from paper_2101_06354_b200 import _native, engine
 
     world, rank, local = dist_env()
+    if world > torch.cuda.device_count():
+        sys.exit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} visible GPU(s)")
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", torch.cuda.current_device())
+    numa = bind_numa(dev.index)  # before any host buffer is allocated or pinned
     lib = _native.load_library()
     cores = host_cores()
 
@@ -364,20 +549,23 @@ def run_b200(args) -> None:
     if rank == 0 and world == 1 and not args.no_cpu:
         n_cpu = cores * args.cpu_pairs_per_core
         pool = CpuBaseline(cores)
-        rate, wall = pool.rate(cpu_pairs(n_cpu, cores))
+        sample = cpu_pairs(n_cpu, cores)
+        rate, wall = pool.rate(sample)
         pool.close()
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+        kind = cpu_kind()
+        what = "ssimkit itself from baseline/_ref" if kind == "reference" else "oracle port of ssimkit's numpy path"
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
                "sample": f"{n_cpu} config-2 pairs ({args.cpu_pairs_per_core} per single-threaded process), "
-                         f"ssim_score + msssim each, oracle port of ssimkit's numpy algorithms, {wall:.1f} s wall"}
+                         f"ssim_score + msssim each, {what}, {wall:.1f} s wall", "host": host_info()}
+        if not args.no_cpu_context:
+            cpu.update(cpu_context(sample[:cores], cores))
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "batch": BATCH, "h": H, "w": W, "window": "gauss 11/1.5",
-                       "levels": LEVELS, "seed_base": 202, "parallelism": f"frame-shard x{world} (weak)",
-                       "l2": "inputs 265 MB per step > 126 MB L2 (no flush needed)"},
+            "config": bench_config(world), "host_binding": numa,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "check": {"msssim_mean": float(scores_host.mean()),
                                                 "ssim_mean": float(ss_terms.score.mean().item())},
@@ -418,8 +606,13 @@ def main() -> None:
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-pairs-per-core", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu-context", action="store_true", help="skip the 1-core / thread-pool CPU figures")
+    ap.add_argument("--launch-selftest", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
-    if args.impl == "reference":
+    relaunch_if_needed(args)
+    if args.launch_selftest:
+        launch_selftest(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_b200(args)

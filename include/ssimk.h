@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SSK_ABI_VERSION 8
+#define SSK_ABI_VERSION 9
 
 /* sample storage types */
 enum {
@@ -92,15 +92,23 @@ typedef struct ssk_planes {
 } ssk_planes;
 
 /* Window (WindowSpec) plus the SSIM constants (SsimConfig.c1/.c2,
- * src/config.py:267-285).  taps = normalised 1-D Gaussian g/sum(g)
- * (gaussian_kernel, src/stats.py:30-44, applied separably). */
+ * src/config.py:267-285).  Gaussian windows (gaussian_kernel, src/stats.py:30-44,
+ * applied separably with the normalised 1-D taps g/sum(g)) are given EITHER by
+ *   sigma > 0 and taps[] all zero: the library builds the taps itself (any odd
+ *     k >= 3 up to SSK_GAUSS_MAX_K), or by
+ *   taps[0..k-1] (k <= 31): the caller's normalised taps, validated -- every tap
+ *     finite and >= 0, taps[i] == taps[k-1-i] exactly, sum within 1e-5 of 1 --
+ *     else SSK_E_ARG (sigma, if also given, is then only informative).
+ * Windows wider than 31 taps need sigma (they run the generic fp64 kernel). */
+#define SSK_GAUSS_MAX_K 255
 typedef struct ssk_window {
   int32_t shape;    /* SSK_RECT or SSK_GAUSS                               */
-  int32_t k;        /* window size (gauss: odd, 3..31; rect: 1..4096)      */
+  int32_t k;        /* window size (gauss: odd, 3..255; rect: 1..4096)     */
   int32_t stride;   /* >= 1                                                */
   int32_t _pad;
   double c1, c2;    /* (k1*L)^2, (k2*L)^2                                  */
-  float taps[32];   /* gauss only                                          */
+  double sigma;     /* gauss: Gaussian sigma (> 0), see above              */
+  float taps[32];   /* gauss, k <= 31: normalised 1-D taps, or all zero    */
 } ssk_window;
 
 /* ------------------------------------------------------------------------ */

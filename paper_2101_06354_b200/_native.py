@@ -32,7 +32,8 @@ RECT, GAUSS = 1, 2
 WANT_Q, WANT_L, WANT_CS, MAP_TERMS, MAP_STATS, WANT_Q2 = 1, 2, 4, 8, 16, 32
 E_ARG, E_WINDOW, E_SHAPE, E_WORKSPACE, E_ALIGN, E_CUDA, E_LEVELS, E_TOO_SMALL = range(-1, -9, -1)
 
-ABI_VERSION = 8
+ABI_VERSION = 9
+GAUSS_MAX_K = 255  # SSK_GAUSS_MAX_K
 
 EXPORTED_SYMBOLS = (
     "ssk_abi_version",
@@ -147,6 +148,7 @@ class Window(ctypes.Structure):
         ("_pad", ctypes.c_int32),
         ("c1", ctypes.c_double),
         ("c2", ctypes.c_double),
+        ("sigma", ctypes.c_double),
         ("taps", ctypes.c_float * 32),
     ]
 
@@ -314,15 +316,18 @@ def make_planes(ref, dist, code: int, bit_depth: int, scale_log2: int = 0) -> Pl
 
 
 def make_window(window, c1: float, c2: float) -> Window:
-    """Window + constants; Gaussian taps are g/sum(g), float64 then rounded to fp32."""
+    """Window + constants.  Gaussian windows carry sigma; up to 31 taps also the taps
+    g/sum(g) (float64, rounded to fp32) for the fp32 kernels, wider windows only sigma
+    (the library builds fp64 taps for its generic kernel)."""
     win = Window(shape=GAUSS if window.shape == "gauss" else RECT, k=window.k, stride=window.stride,
-                 _pad=0, c1=c1, c2=c2)
+                 _pad=0, c1=c1, c2=c2, sigma=0.0)
     if window.shape == "gauss":
-        if window.k > 32:
-            raise ValidationError("gaussian windows wider than 31 taps are not supported on the B200 engine")
-        taps = gaussian_taps(window.sigma, window.k)
-        for i, t in enumerate(taps):
-            win.taps[i] = float(t)
+        if window.k > GAUSS_MAX_K:
+            raise ValidationError(f"gaussian windows wider than {GAUSS_MAX_K} taps are not supported")
+        win.sigma = float(window.sigma)
+        if window.k <= 31:
+            for i, t in enumerate(gaussian_taps(window.sigma, window.k)):
+                win.taps[i] = float(t)
     return win
 
 

@@ -16,7 +16,7 @@ PKG = HERE.parent
 REPO = PKG.parent
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libssimk.so"
-SOURCES = ["gauss_ssim.cu", "gauss_u8.cu", "gauss_u16.cu", "gauss_u32.cu", "gauss_f32.cu", "box_ssim.cu",
+SOURCES = ["gauss_ssim.cu", "gauss_generic.cu", "gauss_u8.cu", "gauss_u16.cu", "gauss_u32.cu", "gauss_f32.cu", "box_ssim.cu",
            "box_block.cu", "volume.cu", "aux_kernels.cu", "pool_adapt.cu", "color_models.cu", "capi.cu"]
 HEADERS = ["common.cuh", "kernels.h", "gauss_ssim.cuh"]
 
@@ -48,8 +48,18 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     obj_dir.mkdir(exist_ok=True)
     cc = nvcc()
 
+    def obj_stale(src: str, obj: Path) -> bool:
+        if force or not obj.exists():
+            return True
+        deps = [HERE / src, HERE / "common.cuh", HERE / "kernels.h", REPO / "include" / "ssimk.h"]
+        if src.startswith("gauss_"):
+            deps.append(HERE / "gauss_ssim.cuh")
+        return any(d.stat().st_mtime > obj.stat().st_mtime for d in deps)
+
     def compile_one(src: str) -> tuple[str, str]:
         obj = obj_dir / (Path(src).stem + ".o")
+        if not obj_stale(src, obj):
+            return str(obj), ""
         cmd = [cc, *ARCH, *FLAGS, "-c", str(HERE / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

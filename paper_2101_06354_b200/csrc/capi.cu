@@ -64,6 +64,7 @@ inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a
 
 struct Plan {
   bool gauss = false;
+  bool generic = false;  // Gaussian wider than 31 taps: the fp64 generic-K kernel (K1g)
   bool box_block = false;
   bool box_int = false;
   bool wide = false;
@@ -71,8 +72,26 @@ struct Plan {
   int gh = 0, gw = 0;
   size_t nparts_per_frame = 0;
   GaussArgs ga{};
+  GaussGenericArgs gg{};
   BoxArgs ba{};
 };
+
+// normalised 1-D Gaussian g/sum(g) in fp64 (gaussian_kernel, src/stats.py:41-44)
+void build_taps(double sigma, int k, double* out) {
+  double sum = 0.0;
+  for (int i = 0; i < k; ++i) {
+    const double c = (double)i - (k - 1) / 2.0;
+    out[i] = std::exp(-(c * c) / (2.0 * sigma * sigma));
+    sum += out[i];
+  }
+  for (int i = 0; i < k; ++i) out[i] /= sum;
+}
+
+bool taps_given(const ssk_window* win) {
+  for (int i = 0; i < 32; ++i)
+    if (win->taps[i] != 0.0f) return true;
+  return false;
+}
 
 int check_planes(const ssk_planes* p) {
   if (!p || !p->ref || !p->dist) return SSK_E_ARG;
@@ -91,8 +110,26 @@ int check_planes(const ssk_planes* p) {
 int check_window(const ssk_planes* p, const ssk_window* win) {
   if (!win || win->k < 1 || win->stride < 1) return SSK_E_ARG;
   if (win->shape == SSK_GAUSS) {
-    if (win->k < 3 || (win->k % 2) == 0 || win->k > 31) return SSK_E_SHAPE;
+    if (win->k < 3 || (win->k % 2) == 0 || win->k > SSK_GAUSS_MAX_K) return SSK_E_SHAPE;
     if (p->dtype == SSK_F64) return SSK_E_ARG;
+    const bool sigma_ok = std::isfinite(win->sigma) && win->sigma > 0.0;
+    if (win->k > 31 || !taps_given(win)) {
+      if (!sigma_ok) return SSK_E_ARG;  // nothing to build the window from
+    } else {
+      // caller's taps: finite, non-negative (a tiny sigma underflows the outer taps to 0,
+      // as in the reference), exactly symmetric, normalised, zero past k
+      double sum = 0.0;
+      for (int i = 0; i < 32; ++i) {
+        const float t = win->taps[i];
+        if (i >= win->k) {
+          if (t != 0.0f) return SSK_E_ARG;
+          continue;
+        }
+        if (!std::isfinite(t) || !(t >= 0.0f) || t != win->taps[win->k - 1 - i]) return SSK_E_ARG;
+        sum += t;
+      }
+      if (std::fabs(sum - 1.0) > 1e-5) return SSK_E_ARG;
+    }
   } else if (win->shape != SSK_RECT) {
     return SSK_E_ARG;
   }
@@ -112,6 +149,37 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
   const double L = std::ldexp(1.0, p->bit_depth) - 1.0;
   const double stored_max = L * std::ldexp(1.0, p->scale_log2);
 
+  if (win->shape == SSK_GAUSS && k > 31) {
+    pl.gauss = pl.generic = true;
+    pl.ga.vcols = 0;  // never joins the fused / multi-level launches
+    GaussGenericArgs& g = pl.gg;
+    g.ref = static_cast<const unsigned char*>(p->ref);
+    g.dist = static_cast<const unsigned char*>(p->dist);
+    g.row_pitch_b = p->row_pitch * es;
+    g.frame_pitch_b = p->frame_pitch * es;
+    g.dtype = p->dtype;
+    g.esize = es;
+    g.n = p->n;
+    g.h = p->h;
+    g.w = p->w;
+    g.k = k;
+    g.stride = s;
+    g.ho = p->h - k + 1;
+    g.wo = p->w - k + 1;
+    g.gh = pl.gh;
+    g.gw = pl.gw;
+    g.seg_rows = 64;
+    g.scale = (p->dtype == SSK_F32) ? 1.0 : std::ldexp(1.0, -p->scale_log2);
+    g.c1 = win->c1;
+    g.c2 = win->c2;
+    g.want = want;
+    g.map_plane = (long long)pl.gh * pl.gw;
+    g.map_frame = g.map_plane * ((want & SSK_MAP_STATS) ? 5 : 3);
+    build_taps(win->sigma, k, g.taps);
+    if (gauss_generic_grid(g.ho, g.wo, p->n, g.seg_rows, &pl.grid)) return SSK_E_ARG;
+    pl.nparts_per_frame = (size_t)pl.grid.x * pl.grid.y;
+    return SSK_OK;
+  }
   if (win->shape == SSK_GAUSS) {
     pl.gauss = true;
     GaussArgs& a = pl.ga;
@@ -178,7 +246,13 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
     // x' = m * 2^-scale with |m| <= 2^(bd+scale) (per-tile shift anywhere in [0, L]): x'^2 is
     // exact in fp32 when m^2 fits 24 bits
     a.exact_sq = (p->dtype != SSK_F32 && p->bit_depth + p->scale_log2 <= 12) ? 1 : 0;
-    std::memcpy(a.taps, win->taps, sizeof(a.taps));
+    if (taps_given(win)) {
+      std::memcpy(a.taps, win->taps, sizeof(a.taps));
+    } else {  // sigma only: the fp64 taps rounded to fp32
+      double t[32];
+      build_taps(win->sigma, k, t);
+      for (int i = 0; i < 32; ++i) a.taps[i] = i < k ? (float)t[i] : 0.0f;
+    }
     pl.grid = dim3(nstrips, nseg, (p->n + 1) / 2);  // two frames per CTA (packed fp32 pairs)
     pl.nparts_per_frame = (size_t)nstrips * nseg;
     a.map_plane = (long long)pl.gh * pl.gw;
@@ -282,6 +356,11 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
 size_t partial_bytes(const Plan& pl, int n) { return align_up(pl.nparts_per_frame * n * 3 * sizeof(double)); }
 
 int run_plan(Plan& pl, double* partials, void* maps, long long* wsums, cudaStream_t st) {
+  if (pl.generic) {
+    pl.gg.partials = partials;
+    pl.gg.maps = maps;
+    return launch_gauss_generic(pl.gg, pl.grid, st);
+  }
   if (pl.gauss) {
     pl.ga.partials = partials;
     pl.ga.maps = maps;
@@ -362,9 +441,11 @@ const char* ssk_strerror(int code) {
 
 size_t ssk_ssim_workspace_bytes(const ssk_planes* p, const ssk_window* win) {
   // enough for any `want`: map launches run on narrower strips (more partials) than
-  // score-only launches, so take the larger of the two plans
+  // score-only launches, and a Σq² launch (rect only) may pick the per-window kernel
+  // (more partials than the block kernel), so take the largest of the plans
   size_t bytes = 0;
-  for (const int want : {SSK_WANT_Q | SSK_WANT_L | SSK_WANT_CS, SSK_WANT_Q | SSK_MAP_TERMS}) {
+  for (const int want : {SSK_WANT_Q | SSK_WANT_L | SSK_WANT_CS, SSK_WANT_Q | SSK_MAP_TERMS,
+                         SSK_WANT_Q | SSK_WANT_Q2}) {
     Plan pl;
     if (plan_ssim(p, win, want, pl)) return 0;
     bytes = std::max(bytes, partial_bytes(pl, p->n) * (pl.gauss ? 1 : 2));  // rect: room for q^2

@@ -20,9 +20,9 @@
 //            ahead of the compute (double buffering), zero fill past the edge.
 //   V pass : thread = input column; converts samples exactly to fp32 (u8/u16
 //            via the 2^23-mantissa splice), subtracts a symmetric shift -- per
-//            tile, the rounded mean of (x + y) / 2 over the tile's middle row
-//            for integer samples, L/2 otherwise (keeps E[x^2]-E[x]^2 well
-//            conditioned in fp32 and preserves exact ref/dist symmetry),
+//            tile, the rounded mean of (x + y) / 2 over the tile's middle row,
+//            for every sample type (keeps E[x^2]-E[x]^2 well conditioned in
+//            fp32 and preserves exact ref/dist symmetry),
 //            forms x, y, x^2, y^2, xy and gathers the
 //            K-tap vertical filter for G output rows (5*G packed accumulators).
 //   H pass : thread = (output row, 8 adjacent columns); K-tap horizontal filter
@@ -242,47 +242,66 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
   const u64 c1_2 = pk(a.c1, a.c1), c2_2 = pk(a.c2, a.c2);
   const u64 two2 = pk(2.f, 2.f), one2 = pk(1.f, 1.f), half2 = pk(0.5f, 0.5f), mhalf2 = pk(-0.5f, -0.5f);
   const u64 twoshift2 = pk(2.f * a.shift, 2.f * a.shift);
-  // Per-tile sample shift (integer inputs): instead of the fixed L/2, every tile shifts its
-  // samples by c = round(mean of (x + y) / 2) over its middle input row, per frame --
-  // symmetric in ref / dist, exact (an integer in stored units), and close to the local
+  // Per-tile sample shift: instead of a fixed L/2, every tile shifts its samples by
+  // c = round(mean of (x + y) / 2) over its middle input row, per frame -- symmetric in
+  // ref / dist, exactly representable (an integer in stored units), and close to the local
   // level, so E[x'^2] - m^2 cancels far less in near-flat windows away from mid-gray.
+  // 8/16-bit samples sum in u32; u32 pyramid levels (up to 2^24 per sample) and float
+  // samples sum in fp64 (fixed shuffle order: bit-identical wherever it is recomputed).
   // vbias / hshift / h2shift carry the tile's shift into the V pass and the epilogue.
-  constexpr bool TSHIFT = ES <= 2;
-  __shared__ unsigned s_tsum[2 * VC / 32][2];
+  constexpr bool TSHIFT = true;
+  using TSum = typename std::conditional<ES == 4, double, unsigned>::type;
+  __shared__ TSum s_tsum[2 * VC / 32][2];
   u64 vbias = bias2, hshift = shift2, h2shift = twoshift2;
-  auto set_shift = [&](const unsigned t0, const unsigned t1) {  // sums of (x + y) over n columns
+  auto set_shift = [&](const TSum t0, const TSum t1) {  // sums of (x + y) over n columns
     const unsigned n = (unsigned)max(1, min(TWI, a.w - c0));
-    const float sc = a.conv_scale;                        // 2^-scale_log2 (exact)
-    const float cv0 = (float)((t0 + n) / (2u * n)) * sc;  // value units, exact
-    const float cv1 = (float)((t1 + n) / (2u * n)) * sc;
-    const float base = -8388608.f * sc;                   // the 2^23 splice, in value units
-    vbias = pk(base - cv0, base - cv1);                   // exact: (2^23 + c_stored) * 2^-k
-    hshift = pk(cv0, cv1);
-    h2shift = pk(2.f * cv0, 2.f * cv1);
+    const float sc = a.conv_scale;                        // 2^-scale_log2 (exact); 1 for floats
+    if constexpr (ES == 4) {
+      const float cv0 = (float)floor(t0 / (2.0 * n) + 0.5) * sc;  // integer (stored units): exact
+      const float cv1 = (float)floor(t1 / (2.0 * n) + 0.5) * sc;
+      vbias = pk(-cv0, -cv1);                             // x' = fma(x, sc, -c), one rounding
+      hshift = pk(cv0, cv1);
+      h2shift = pk(2.f * cv0, 2.f * cv1);
+    } else {
+      const float cv0 = (float)((t0 + n) / (2u * n)) * sc;  // value units, exact
+      const float cv1 = (float)((t1 + n) / (2u * n)) * sc;
+      const float base = -8388608.f * sc;                   // the 2^23 splice, in value units
+      vbias = pk(base - cv0, base - cv1);                   // exact: (2^23 + c_stored) * 2^-k
+      hshift = pk(cv0, cv1);
+      h2shift = pk(2.f * cv0, 2.f * cv1);
+    }
+  };
+  auto stored = [](const unsigned char* p) -> TSum {  // one stored sample, as summed
+    if constexpr (ES == 1) return (unsigned)*p;
+    else if constexpr (ES == 2) return (unsigned)*reinterpret_cast<const unsigned short*>(p);
+    else if constexpr (std::is_same<TIN, float>::value) return (double)*reinterpret_cast<const float*>(p);
+    else return (double)*reinterpret_cast<const unsigned*>(p);
+  };
+  auto warp_total = [](TSum v) -> TSum {
+    if constexpr (ES == 4) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      return v;
+    } else {
+      return __reduce_add_sync(0xffffffffu, v);
+    }
   };
   auto tile_shift = [&](const int gt, const int gs, const int wbase, auto&& gsync) {
     const int r = min(y0 + (y1 - y0) / 2 + K / 2, a.h - 1);
-    unsigned v0 = 0u, v1 = 0u;
+    TSum v0 = 0, v1 = 0;
     for (int i = gt; i < TWI && c0 + i < a.w; i += gs) {
       const long long off = (long long)r * a.row_pitch_b + (long long)(c0 + i) * ES;
-      if constexpr (ES == 1) {
-        v0 += (unsigned)a.ref[fo0 + off] + a.dist[fo0 + off];
-        v1 += (unsigned)a.ref[fo1 + off] + a.dist[fo1 + off];
-      } else {
-        v0 += (unsigned)*reinterpret_cast<const unsigned short*>(a.ref + fo0 + off) +
-              *reinterpret_cast<const unsigned short*>(a.dist + fo0 + off);
-        v1 += (unsigned)*reinterpret_cast<const unsigned short*>(a.ref + fo1 + off) +
-              *reinterpret_cast<const unsigned short*>(a.dist + fo1 + off);
-      }
+      v0 += stored(a.ref + fo0 + off) + stored(a.dist + fo0 + off);
+      v1 += stored(a.ref + fo1 + off) + stored(a.dist + fo1 + off);
     }
-    v0 = __reduce_add_sync(0xffffffffu, v0);
-    v1 = __reduce_add_sync(0xffffffffu, v1);
+    v0 = warp_total(v0);
+    v1 = warp_total(v1);
     if ((gt & 31) == 0) {
       s_tsum[wbase + (gt >> 5)][0] = v0;
       s_tsum[wbase + (gt >> 5)][1] = v1;
     }
     gsync();
-    unsigned t0 = 0u, t1 = 0u;
+    TSum t0 = 0, t1 = 0;
     for (int wi = 0; wi < gs / 32; ++wi) {
       t0 += s_tsum[wbase + wi][0];
       t1 += s_tsum[wbase + wi][1];
@@ -296,26 +315,19 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
   auto chunk_shift_smem = [&](const int c) {
     const int row = min(y0 + c * G + (G + K - 1) / 2, in_end - 1);
     const unsigned char* rp = raw + (((row - y0) % RR) * 4) * RB + tid * ES;
-    unsigned v0 = 0u, v1 = 0u;
+    TSum v0 = 0, v1 = 0;
     if (tid < TWI && c0 + tid < a.w) {
-      if constexpr (ES == 1) {
-        v0 = (unsigned)rp[0] + rp[2 * RB];
-        v1 = (unsigned)rp[RB] + rp[3 * RB];
-      } else {
-        v0 = (unsigned)*reinterpret_cast<const unsigned short*>(rp) +
-             *reinterpret_cast<const unsigned short*>(rp + 2 * RB);
-        v1 = (unsigned)*reinterpret_cast<const unsigned short*>(rp + RB) +
-             *reinterpret_cast<const unsigned short*>(rp + 3 * RB);
-      }
+      v0 = stored(rp) + stored(rp + 2 * RB);
+      v1 = stored(rp + RB) + stored(rp + 3 * RB);
     }
-    v0 = __reduce_add_sync(0xffffffffu, v0);
-    v1 = __reduce_add_sync(0xffffffffu, v1);
+    v0 = warp_total(v0);
+    v1 = warp_total(v1);
     if ((tid & 31) == 0) {
       s_tsum[tid >> 5][0] = v0;
       s_tsum[tid >> 5][1] = v1;
     }
     __syncthreads();
-    unsigned t0 = 0u, t1 = 0u;
+    TSum t0 = 0, t1 = 0;
     for (int wi = 0; wi < NT / 32; ++wi) {
       t0 += s_tsum[wi][0];
       t1 += s_tsum[wi][1];

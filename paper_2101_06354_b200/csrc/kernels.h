@@ -59,6 +59,27 @@ int launch_gauss_u16(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 int launch_gauss_u32(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 int launch_gauss_f32(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 
+// ---------------- K1g: Gaussian windows wider than 31 taps (fp64, generic K) ----------------
+struct GaussGenericArgs {
+  const unsigned char* ref;
+  const unsigned char* dist;
+  long long row_pitch_b, frame_pitch_b;  // bytes
+  int dtype, esize;
+  int n, h, w, k, stride;
+  int ho, wo, gh, gw;
+  int seg_rows;                // output rows per segment (gridDim.y segments)
+  double scale;                // stored integer sample -> value (2^-scale_log2); 1 for f32
+  double c1, c2;
+  int want;
+  double* partials;            // [n][gridDim.y][gridDim.x][3]
+  void* maps;                  // float32 [n][planes][gh][gw]
+  long long map_plane, map_frame;
+  double taps[255];            // normalised 1-D taps g/sum(g), built in fp64 from sigma
+};
+size_t gauss_generic_smem(int k);
+int gauss_generic_grid(int ho, int wo, int n, int seg_rows, dim3* grid);
+int launch_gauss_generic(const GaussGenericArgs& a, dim3 grid, cudaStream_t st);
+
 // ---------------- K2: rect window ----------------
 constexpr int BX_THREADS = 128;  // one input column per thread in the V pass
 

@@ -397,11 +397,13 @@ __global__ void __launch_bounds__(PL_THREADS) select_pick_kernel(const __grid_co
       if (lane >= o) incl += v;
     }
     if (lane == 31) wtot[warp] = incl;
+    // every thread reads the residual rank before the barrier: the owning thread
+    // rewrites st[1] below, and no other thread may see the new value
+    const unsigned long long k = st[1];
     __syncthreads();
     unsigned long long base = 0;
     for (int wi = 0; wi < warp; ++wi) base += wtot[wi];
     const unsigned long long excl = base + incl - s;
-    const unsigned long long k = st[1];
     if (s > 0 && k >= excl && k < excl + s) {
       unsigned long long cum = excl;
 #pragma unroll

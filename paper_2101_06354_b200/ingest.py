@@ -10,6 +10,8 @@ chroma tags and error classes follow the reference readers.
 
 from __future__ import annotations
 
+import contextlib
+
 import os
 from dataclasses import dataclass
 from typing import Iterator, Optional, Sequence
@@ -398,7 +400,25 @@ def score_files(ref: FrameSource, dist: FrameSource, config=None, batch_frames: 
         raise ValidationError(f"streams differ in length: {len(ref)} vs {len(dist)} frames")
     cfg = config.for_bit_depth(ref.header.bit_depth)
     scorer = SequenceScorer(cfg, batch_frames, color_weights)
-    direct = ref.pin() and dist.pin()  # page-locked mappings: planes DMA'd with no host copy
-    if color_weights is not None:
-        return scorer.score(ref.frames(), dist.frames(), direct=direct)
-    return scorer.score(ref.luma(), dist.luma(), direct=direct)
+    with pinned_pair(ref, dist) as direct:  # page-locked mappings: planes DMA'd with no host copy
+        if color_weights is not None:
+            return scorer.score(ref.frames(), dist.frames(), direct=direct)
+        return scorer.score(ref.luma(), dist.luma(), direct=direct)
+
+
+@contextlib.contextmanager
+def pinned_pair(ref: FrameSource, dist: FrameSource):
+    """Page-lock both mappings for the duration of the block (yields whether both are pinned);
+    always unpins what it pinned, also when the second pin fails or scoring raises."""
+    pinned = []
+    try:
+        for src in (ref, dist):
+            if src.pinned:
+                continue
+            if not src.pin():
+                break
+            pinned.append(src)
+        yield ref.pinned and dist.pinned
+    finally:
+        for src in pinned:
+            src.unpin()

@@ -320,8 +320,11 @@ def run_score(ref_path, dist_path, spec: PipelineSpec, *, width: Optional[int] =
             from .video import SequenceScorer
 
             cfg = config.for_bit_depth(ref.header.bit_depth)
-            direct = ref.source.pin() and dist.source.pin()  # DMA straight from the page-locked mapping
-            seq = SequenceScorer(cfg, batch_frames).score(ref.source.luma(), dist.source.luma(), direct=direct)
+            from .ingest import pinned_pair
+
+            with pinned_pair(ref.source, dist.source) as direct:  # DMA straight from page-locked mappings
+                seq = SequenceScorer(cfg, batch_frames).score(ref.source.luma(), dist.source.luma(),
+                                                              direct=direct)
             results = [FrameScore(r.score, r.am, r.l_mean, r.cs_mean) for r in seq.records]
         elif spec.kt > 1 and config.multiscale.enabled:
             series = msssim3d(_luma_iter(ref), _luma_iter(dist), spec.kt, config.multiscale, config)

@@ -767,3 +767,166 @@ def test_gaussian_letterbox_bars_vs_oracle(cuda, oracle, bar):
         assert np.max(np.abs(g - w_)) < MAP_TOL
     terms = P.ssim_terms(a, b, cfg)
     assert max(abs(x - y) for x, y in zip(terms, oracle.ssim_terms(a, b, **win))) < SCORE_TOL
+
+
+@pytest.mark.parametrize("k,s", [(8, 4), (8, 2), (11, 1)])
+def test_workspace_query_covers_q2_launches(cuda, oracle, k, s):
+    """A Σq² launch (CoV / MD(2) pooling, rect windows) may take the per-window kernel, which
+    makes more partials than the block kernel the score-only plan picks: a workspace of
+    exactly the queried size must still work (1080p, rect 8 stride 4, cov)."""
+    import ctypes
+
+    import torch
+    from paper_2101_06354_b200 import _native as nat
+
+    rng = np.random.default_rng(k * 10 + s)
+    h, w = 1080, 1920
+    a_np = rng.integers(0, 256, (1, h, w)).astype(np.uint8)
+    b_np = np.clip(a_np.astype(int) + rng.integers(-30, 31, a_np.shape), 0, 255).astype(np.uint8)
+    a, b = torch.from_numpy(a_np).cuda(), torch.from_numpy(b_np).cuda()
+    pair = engine.device_pair(a, b, 8, gauss=False)
+    window = P.WindowSpec.rectangular(k, stride=s)
+    cfg = P.SsimConfig(window=window)
+    lib = nat.lib()
+    planes, win = pair.planes(), nat.make_window(window, cfg.c1, cfg.c2)
+    size = lib.ssk_ssim_workspace_bytes(ctypes.byref(planes), ctypes.byref(win))
+    ws = torch.empty(size, dtype=torch.uint8, device="cuda")
+    sums = torch.empty((1, 4), dtype=torch.float64, device="cuda")
+    rc = lib.ssk_ssim(ctypes.byref(planes), ctypes.byref(win), nat.WANT_Q | nat.WANT_Q2, sums.data_ptr(),
+                      None, ws.data_ptr(), ws.numel(), nat.stream_handle(None))
+    assert rc == 0, nat.lib().ssk_strerror(rc)
+    q = oracle.ssim_maps(a_np[0], b_np[0], shape="rect", k=k, stride=s)[2]
+    got = sums.cpu().numpy()[0]
+    assert abs(got[0] - q.sum()) < 1e-9 * q.size and abs(got[3] - (q * q).sum()) < 1e-9 * q.size
+
+
+@pytest.mark.parametrize("sigma,k,stride,bd,kind", [
+    (6.0, 37, 1, 8, "u8"), (6.0, 37, 3, 8, "u8"), (10.0, 61, 1, 10, "u16"), (5.5, 35, 2, 8, "f32"),
+])
+def test_wide_gaussian_windows_vs_oracle(cuda, oracle, sigma, k, stride, bd, kind):
+    """Gaussian windows wider than 31 taps (the reference accepts any odd k >= 3,
+    src/config.py:55-56): the generic fp64 kernel, maps and scores against the oracle,
+    strided grids equal to dense[::s, ::s] exactly."""
+    from paper_2101_06354_b200 import synth
+
+    rng = np.random.default_rng(k * 7 + stride)
+    peak = (1 << bd) - 1
+    h, w = 150, 230
+    a = synth.inv_f_noise(rng, h, w, float(peak))
+    b = np.clip(a + rng.normal(0.0, peak / 40.0, a.shape), 0, peak)
+    if kind == "f32":
+        a, b = (a * 0.99 + 0.3).astype(np.float32), b.astype(np.float32)
+    else:
+        dt = np.uint8 if kind == "u8" else np.uint16
+        a, b = a.astype(dt), np.round(b).astype(dt)
+    window = P.WindowSpec.gaussian(sigma, k=k, stride=stride)
+    cfg = P.SsimConfig(bit_depth=bd, window=window)
+    ra, rb = P.LumaPlane(a, bd), P.LumaPlane(b, bd)
+    maps = P.ssim_map(ra, rb, cfg)
+    win = dict(shape="gauss", k=k, sigma=sigma, stride=stride, bit_depth=bd)
+    wl, wcs, wq = oracle.ssim_maps(a, b, **win)
+    assert maps.q_map.values.shape == wq.shape
+    for got, want in ((maps.l_map.values, wl), (maps.cs_map.values, wcs), (maps.q_map.values, wq)):
+        assert np.max(np.abs(got - want)) < 1e-6   # fp64 kernel, fp32 map store
+    terms = P.ssim_terms(ra, rb, cfg)
+    assert max(abs(x - y) for x, y in zip(terms, oracle.ssim_terms(a, b, **win))) < 1e-9
+    st = P.local_statistics(ra, rb, window)
+    want_st = oracle.local_statistics(a, b, "gauss", k, stride, sigma)
+    assert np.max(np.abs(st.mu1 - want_st[0])) < 1e-3 * peak / 255
+    assert np.max(np.abs(st.cov - want_st[4])) < 1e-2 * (peak / 255) ** 2
+    if stride > 1:
+        dense = P.ssim_map(ra, rb, P.SsimConfig(bit_depth=bd, window=P.WindowSpec.gaussian(sigma, k=k))).q_map.values
+        assert np.array_equal(dense[::stride, ::stride], maps.q_map.values)
+
+
+def test_wide_gaussian_msssim_vs_oracle(cuda, oracle):
+    """MS-SSIM with a 37-tap window: every level on the generic kernel (no fused level 1)."""
+    from paper_2101_06354_b200 import synth
+
+    rng = np.random.default_rng(37)
+    a = synth.inv_f_noise(rng, 160, 300, 255.0).astype(np.uint8)
+    b = np.clip(a.astype(int) + rng.integers(-20, 21, a.shape), 0, 255).astype(np.uint8)
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(6.0))
+    got = P.scale_scores(a, b, cfg, 2)
+    want = oracle.scale_scores(a, b, 2, shape="gauss", k=37, sigma=6.0)
+    assert np.max(np.abs(np.array(got) - np.array(want))) < 1e-9
+    import torch
+
+    ms = P.msssim_batch(torch.from_numpy(a[None]).cuda(), torch.from_numpy(b[None]).cuda(), cfg,
+                        P.MultiscaleSpec.product(2))
+    assert abs(float(ms[0]) - oracle.msssim(a, b, 2, shape="gauss", k=37, sigma=6.0)) < 1e-9
+
+
+def _float_adversarial():
+    h, w = 160, 520
+    yy, xx = np.mgrid[0:h, 0:w]
+    rng = np.random.default_rng(99)
+    grad = (18.0 + 4.0 * xx / (w - 1)).astype(np.float32)            # near-flat, mu ~ 20
+    from paper_2101_06354_b200 import synth
+
+    content = synth.inv_f_noise(rng, h, w, 255.0).astype(np.float32)
+    bars = content.copy()
+    bars[:60] = rng.uniform(0.0, 2.0, (60, w)).astype(np.float32)    # dark letterbox bar
+    bright = np.full((h, w), 236.0, np.float32) + rng.uniform(0, 0.5, (h, w)).astype(np.float32)
+    return {
+        "gradient_mu20": (grad, (grad + np.float32(0.37)).astype(np.float32)),
+        "letterbox": (bars, np.clip(bars + rng.normal(0, 0.3, bars.shape), 0, 255).astype(np.float32)),
+        "bright_flat": (bright, np.clip(bright + rng.normal(0, 0.2, bright.shape), 0, 255).astype(np.float32)),
+    }
+
+
+@pytest.mark.parametrize("name", sorted(_float_adversarial()))
+def test_float_input_adversarial_vs_oracle(cuda, oracle, name):
+    """float32 samples get the per-tile symmetric shift too (was a fixed L/2: a near-flat
+    gradient at mu ~ 20 cancelled in fp32, 1.4e-4 off in cs): maps within 1e-4, scores
+    and 3-scale MS-SSIM within 1e-5 of the float64 oracle."""
+    a, b = _float_adversarial()[name]
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    win = dict(shape="gauss", k=11, sigma=1.5)
+    got = P.ssim_map(a, b, cfg)
+    for g, w_ in zip((got.l_map.values, got.cs_map.values, got.q_map.values), oracle.ssim_maps(a, b, **win)):
+        assert np.max(np.abs(g - w_)) < MAP_TOL
+    terms = P.ssim_terms(a, b, cfg)
+    assert max(abs(x - y) for x, y in zip(terms, oracle.ssim_terms(a, b, **win))) < SCORE_TOL
+    assert abs(P.msssim(a, b, cfg, P.MultiscaleSpec.product(3)) - oracle.msssim(a, b, 3, **win)) < SCORE_TOL
+
+
+@pytest.mark.parametrize("bar", [0, 120])
+def test_10bit_msssim_dark_letterbox_u32_level(cuda, oracle, bar):
+    """10-bit 5-scale MS-SSIM: the coarsest level holds u32 sums of 256 samples (the per-tile
+    shift now covers u32 levels); a dark near-flat letterbox bar above the content."""
+    from paper_2101_06354_b200 import synth
+
+    rng = np.random.default_rng(1000 + bar)
+    h, w = 480, 704
+    a = synth.inv_f_noise(rng, h, w, 1023.0)
+    if bar:
+        a[:bar] = rng.integers(0, 4, (bar, w))
+    b = np.clip(a + rng.integers(-2, 3, a.shape), 0, 1023)
+    a, b = a.astype(np.uint16), b.astype(np.uint16)
+    cfg = P.SsimConfig(bit_depth=10, window=P.WindowSpec.gaussian(1.5))
+    win = dict(shape="gauss", k=11, sigma=1.5, bit_depth=10)
+    ra, rb = P.LumaPlane(a, 10), P.LumaPlane(b, 10)
+    got = P.scale_scores(ra, rb, cfg, 5)
+    want = oracle.scale_scores(a, b, 5, **win)
+    assert np.max(np.abs(np.array(got) - np.array(want))) < SCORE_TOL
+
+
+def test_score_only_bright_middle_row_over_dark(cuda, oracle):
+    """score-only launches shift per tile from the tile's middle row; a bright band
+    there over dark, near-flat content is the worst case for that choice (shift ~ L away
+    from the dark windows' level).  Scores within 1e-5 of the oracle, and the score-only
+    path agrees with the map path's mean."""
+    rng = np.random.default_rng(5)
+    h, w = 300, 520
+    a = rng.integers(0, 3, (h, w)).astype(np.uint8)
+    for r0 in (44, 140, 240):                      # near every segment's middle row
+        a[r0:r0 + 16] = 250 + rng.integers(0, 5, (16, w))
+    b = np.clip(a.astype(int) + rng.integers(-1, 2, a.shape), 0, 255).astype(np.uint8)
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    win = dict(shape="gauss", k=11, sigma=1.5)
+    terms = P.ssim_terms(a, b, cfg)
+    want = oracle.ssim_terms(a, b, **win)
+    assert max(abs(x - y) for x, y in zip(terms, want)) < SCORE_TOL
+    q = P.ssim_map(a, b, cfg).q_map.values
+    assert abs(float(q.mean()) - terms[0]) < SCORE_TOL

@@ -85,6 +85,7 @@ def test_ctypes_struct_layout_matches_header(tmp_path):
         '#include <stdio.h>\n#include <stddef.h>\n#include "ssimk.h"\n'
         "int main(void){printf(\"%zu %zu %zu %zu %zu %zu\\n\", sizeof(ssk_planes), offsetof(ssk_planes,row_pitch),"
         " offsetof(ssk_planes,frame_pitch), sizeof(ssk_window), offsetof(ssk_window,c1), offsetof(ssk_window,taps));"
+        "printf(\"%zu\\n\", offsetof(ssk_window,sigma));"
         "return 0;}\n"
     )
     exe = tmp_path / "layout"
@@ -92,5 +93,59 @@ def test_ctypes_struct_layout_matches_header(tmp_path):
     vals = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
     assert vals == [
         ctypes.sizeof(nat.Planes), nat.Planes.row_pitch.offset, nat.Planes.frame_pitch.offset,
-        ctypes.sizeof(nat.Window), nat.Window.c1.offset, nat.Window.taps.offset,
+        ctypes.sizeof(nat.Window), nat.Window.c1.offset, nat.Window.taps.offset, nat.Window.sigma.offset,
     ]
+
+
+def _gauss_call(win, h=64, w=64):
+    lib = nat.load_library()
+    pitch = (w + 15) // 16 * 16
+    p = nat.Planes(ref=256, dist=512, dtype=nat.U8, n=1, h=h, w=w, bit_depth=8, row_pitch=pitch,
+                   frame_pitch=pitch * h)
+    return lib.ssk_ssim_workspace_bytes(ctypes.byref(p), ctypes.byref(win))
+
+
+def _gauss_window(k=11, sigma=0.0, taps=None):
+    win = nat.Window(shape=nat.GAUSS, k=k, stride=1, c1=6.5025, c2=58.5225, sigma=sigma)
+    for i, t in enumerate(taps if taps is not None else []):
+        win.taps[i] = float(t)
+    return win
+
+
+def test_gaussian_window_taps_are_validated():
+    """ABI v9: a Gaussian window needs sigma or valid taps.  Zero taps without sigma (a binding
+    that forgot them), negative, asymmetric or unnormalised taps are rejected (planning
+    fails -> workspace query 0 / SSK_E_ARG) instead of silently scoring q = 1."""
+    good = nat.gaussian_taps(1.5, 11)
+    assert _gauss_call(_gauss_window(taps=good)) > 0
+    assert _gauss_call(_gauss_window(sigma=1.5)) > 0            # library builds the taps
+    assert _gauss_call(_gauss_window()) == 0                     # neither
+    asym = good.copy()
+    asym[0] *= 1.01
+    asym /= asym.sum()
+    assert _gauss_call(_gauss_window(taps=asym)) == 0
+    assert _gauss_call(_gauss_window(taps=good * 2.0)) == 0      # not normalised
+    neg = good.copy()
+    neg[0] = neg[-1] = -neg[0]
+    assert _gauss_call(_gauss_window(taps=neg)) == 0
+    extra = list(good) + [0.01]                                  # non-zero past k
+    assert _gauss_call(_gauss_window(taps=extra)) == 0
+    assert _gauss_call(_gauss_window(sigma=-1.0)) == 0
+    lib = nat.load_library()
+    p = nat.Planes(ref=256, dist=512, dtype=nat.U8, n=1, h=64, w=64, bit_depth=8, row_pitch=64, frame_pitch=4096)
+    rc = lib.ssk_ssim(ctypes.byref(p), ctypes.byref(_gauss_window()), 1, ctypes.c_void_p(64), None, None, 0, None)
+    assert rc == nat.E_ARG
+
+
+def test_wide_gaussian_windows_plan_with_sigma():
+    """k > 31 (sigma > 5 at the default size): planned on the generic kernel from sigma alone;
+    taps cannot carry them; k above SSK_GAUSS_MAX_K is a shape error."""
+    from paper_2101_06354_b200.options import WindowSpec
+
+    w37 = nat.make_window(WindowSpec.gaussian(6.0), 6.5025, 58.5225)
+    assert w37.k == 37 and w37.sigma == 6.0 and all(t == 0.0 for t in w37.taps)
+    assert _gauss_call(w37, 200, 300) > 0
+    assert _gauss_call(_gauss_window(k=37), 200, 300) == 0       # no sigma
+    assert _gauss_call(_gauss_window(k=257, sigma=40.0), 300, 300) == 0
+    assert _gauss_call(_gauss_window(k=255, sigma=40.0), 300, 300) > 0
+    assert _gauss_call(_gauss_window(k=37, sigma=6.0), 30, 300) == 0   # window larger than image
