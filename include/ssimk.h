@@ -56,8 +56,12 @@ enum {
   SSK_WANT_CS = 4,     /* per-frame sum of cs                                 */
   SSK_MAP_TERMS = 8,   /* write the l, cs, q maps (3 planes per frame)        */
   SSK_MAP_STATS = 16,  /* write mu1, mu2, var1, var2, cov (5 planes per frame) */
-  SSK_WANT_Q2 = 32     /* rect windows: also the per-frame sum of q^2, d_sums is then
+  SSK_WANT_Q2 = 32,    /* rect windows: also the per-frame sum of q^2, d_sums is then
                           [n][4] (CoV / MD(2) pooling without a map, src/pooling.py:157-166) */
+  SSK_MAP_F64 = 64     /* Gaussian windows: maps (and sums) from the fp64 kernel, maps stored
+                          as float64 -- the reference's own precision, for the map API
+                          (ssim_map / local_statistics); without it Gaussian maps are the
+                          fp32 kernel's, stored as float32 */
 };
 
 /* error codes */
@@ -130,7 +134,8 @@ size_t ssk_msssim_workspace_bytes(const ssk_planes* p, const ssk_window* win, in
  *             (only the components selected by `want` are meaningful).
  *   d_maps  : optional; SSK_MAP_TERMS -> [n][3][gh][gw] (l, cs, q),
  *             SSK_MAP_STATS -> [n][5][gh][gw] (mu1, mu2, var1, var2, cov);
- *             float32 for Gaussian windows, float64 for rect windows.
+ *             float32 for Gaussian windows (float64 with SSK_MAP_F64), float64 for
+ *             rect windows.
  * Rect windows on integer samples use exact integer window sums (the
  * integral engine's int64 arithmetic, src/stats.py:101-103) and a float64
  * epilogue in the reference's operation order, so their maps are

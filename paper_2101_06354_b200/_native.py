@@ -9,6 +9,7 @@ rather than silently compute on the host).
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 from typing import Optional
@@ -24,12 +25,13 @@ from .errors import (
     WindowLargerThanImage,
 )
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libssimk.so"
+# SSK_LIBRARY overrides the library path (tools/sync_stress.py loads the stress build this way)
+LIB_PATH = Path(os.environ.get("SSK_LIBRARY") or Path(__file__).resolve().parent / "_lib" / "libssimk.so")
 
 # enums (include/ssimk.h)
 U8, U16, U32, F32, F64 = 1, 2, 3, 4, 5
 RECT, GAUSS = 1, 2
-WANT_Q, WANT_L, WANT_CS, MAP_TERMS, MAP_STATS, WANT_Q2 = 1, 2, 4, 8, 16, 32
+WANT_Q, WANT_L, WANT_CS, MAP_TERMS, MAP_STATS, WANT_Q2, MAP_F64 = 1, 2, 4, 8, 16, 32, 64
 E_ARG, E_WINDOW, E_SHAPE, E_WORKSPACE, E_ALIGN, E_CUDA, E_LEVELS, E_TOO_SMALL = range(-1, -9, -1)
 
 ABI_VERSION = 9

@@ -313,7 +313,9 @@ __global__ void __launch_bounds__(128) box_bulk_kernel(const __grid_constant__ B
       const int br = base + rr;
       if (br < nrows) {
         const int stage = br % ST;
+        SSK_JITTER(200);
         mbar_wait(&bar[stage], (uint32_t)((br / ST) & 1));
+        SSK_JITTER(201);
         uint32_t vx[S][4], vy[S][4];
         const unsigned char* sb = wbuf + stage * STAGEB + delta + lane * 8 * ES;
 #pragma unroll
@@ -333,7 +335,12 @@ __global__ void __launch_bounds__(128) box_bulk_kernel(const __grid_constant__ B
           }
         }
         __syncwarp();  // every lane has its samples: the stage can be refilled
-        if (lane == 0 && br + ST < nrows) issue(br + ST, stage);
+        if (lane == 0 && br + ST < nrows) {
+          SSK_JITTER(202);
+          // order the warp's generic-proxy reads of this stage before the async-proxy refill
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(br + ST, stage);
+        }
         uint32_t sx[NB] = {}, sy[NB] = {}, xx[NB] = {}, yy[NB] = {}, xy[NB] = {};
 #pragma unroll
         for (int r = 0; r < S; ++r) {

@@ -16,9 +16,9 @@ PKG = HERE.parent
 REPO = PKG.parent
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libssimk.so"
-SOURCES = ["gauss_ssim.cu", "gauss_generic.cu", "gauss_u8.cu", "gauss_u16.cu", "gauss_u32.cu", "gauss_f32.cu", "box_ssim.cu",
+SOURCES = ["gauss_ssim.cu", "gauss_generic.cu", "gauss_stride.cu", "gauss_stride_s2.cu", "gauss_stride_s3.cu", "gauss_stride_s4.cu", "gauss_stride_s5.cu", "gauss_stride_s6.cu", "gauss_stride_s7.cu", "gauss_stride_s8.cu", "gauss_u8.cu", "gauss_u16.cu", "gauss_u32.cu", "gauss_f32.cu", "box_ssim.cu",
            "box_block.cu", "volume.cu", "aux_kernels.cu", "pool_adapt.cu", "color_models.cu", "capi.cu"]
-HEADERS = ["common.cuh", "kernels.h", "gauss_ssim.cuh"]
+HEADERS = ["common.cuh", "kernels.h", "gauss_ssim.cuh", "gauss_stride.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
@@ -32,35 +32,39 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found: the B200 engine has no CPU fallback")
 
 
-def _stale() -> bool:
-    if not LIB.exists():
+def _stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     deps = [HERE / s for s in SOURCES + HEADERS] + [REPO / "include" / "ssimk.h"]
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return LIB
-    OUT_DIR.mkdir(exist_ok=True)
-    obj_dir = OUT_DIR / "obj"
+def build(force: bool = False, verbose: bool = False, stress: bool = False) -> Path:
+    """stress=True: the synchronisation-stress variant (-DSSK_SYNC_STRESS, random warp delays at
+    every barrier hand-off) into _lib/stress/libssimk.so, for tools/sync_stress.py only."""
+    lib_out = OUT_DIR / "stress" / "libssimk.so" if stress else LIB
+    if not force and not _stale(lib_out):
+        return lib_out
+    lib_out.parent.mkdir(parents=True, exist_ok=True)
+    obj_dir = OUT_DIR / ("obj_stress" if stress else "obj")
     obj_dir.mkdir(exist_ok=True)
     cc = nvcc()
+    extra = ["-DSSK_SYNC_STRESS"] if stress else []
 
     def obj_stale(src: str, obj: Path) -> bool:
         if force or not obj.exists():
             return True
         deps = [HERE / src, HERE / "common.cuh", HERE / "kernels.h", REPO / "include" / "ssimk.h"]
         if src.startswith("gauss_"):
-            deps.append(HERE / "gauss_ssim.cuh")
+            deps += [HERE / "gauss_ssim.cuh", HERE / "gauss_stride.cuh"]
         return any(d.stat().st_mtime > obj.stat().st_mtime for d in deps)
 
     def compile_one(src: str) -> tuple[str, str]:
         obj = obj_dir / (Path(src).stem + ".o")
         if not obj_stale(src, obj):
             return str(obj), ""
-        cmd = [cc, *ARCH, *FLAGS, "-c", str(HERE / src), "-o", str(obj)]
+        cmd = [cc, *ARCH, *FLAGS, *extra, "-c", str(HERE / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
@@ -72,15 +76,14 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if verbose:
         for _, log in results:
             sys.stderr.write(log)
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib_out.with_suffix(".so.tmp")
     cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose=True, stress="--stress" in sys.argv))

@@ -65,6 +65,7 @@ inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a
 struct Plan {
   bool gauss = false;
   bool generic = false;  // Gaussian wider than 31 taps: the fp64 generic-K kernel (K1g)
+  bool strided = false;  // strided Gaussian scores: the anchor-only kernel (K1s)
   bool box_block = false;
   bool box_int = false;
   bool wide = false;
@@ -149,7 +150,7 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
   const double L = std::ldexp(1.0, p->bit_depth) - 1.0;
   const double stored_max = L * std::ldexp(1.0, p->scale_log2);
 
-  if (win->shape == SSK_GAUSS && k > 31) {
+  if (win->shape == SSK_GAUSS && (k > 31 || (want & SSK_MAP_F64))) {
     pl.gauss = pl.generic = true;
     pl.ga.vcols = 0;  // never joins the fused / multi-level launches
     GaussGenericArgs& g = pl.gg;
@@ -175,7 +176,12 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
     g.want = want;
     g.map_plane = (long long)pl.gh * pl.gw;
     g.map_frame = g.map_plane * ((want & SSK_MAP_STATS) ? 5 : 3);
-    build_taps(win->sigma, k, g.taps);
+    g.map_f64 = (want & SSK_MAP_F64) ? 1 : 0;
+    if (win->sigma > 0.0) {
+      build_taps(win->sigma, k, g.taps);
+    } else {  // caller's fp32 taps (k <= 31), widened
+      for (int i = 0; i < k; ++i) g.taps[i] = (double)win->taps[i];
+    }
     if (gauss_generic_grid(g.ho, g.wo, p->n, g.seg_rows, &pl.grid)) return SSK_E_ARG;
     pl.nparts_per_frame = (size_t)pl.grid.x * pl.grid.y;
     return SSK_OK;
@@ -257,6 +263,24 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
     pl.nparts_per_frame = (size_t)nstrips * nseg;
     a.map_plane = (long long)pl.gh * pl.gw;
     a.map_frame = a.map_plane * ((want & SSK_MAP_STATS) ? 5 : 3);
+    // strided score launches on 8/16-bit samples: the anchor-only kernel (K1s); map
+    // launches stay on K1 (strided maps == dense maps at [::s, ::s], bit-exact)
+    static const int stride_fast = [] {
+      const char* e = std::getenv("SSK_STRIDE_FAST");  // default on; 0 = K1 with anchor masking
+      return e ? std::atoi(e) : 1;
+    }();
+    if (!maps && stride_fast && gauss_stride_supported(p->dtype, k, s)) {
+      pl.strided = true;
+      a.vcols = 0;  // never joins the fused / multi-level launches
+      const int twa = gauss_stride_twa(k, s, es);
+      const int sx = (pl.gw + twa - 1) / twa;
+      int sseg = (pl.gh + 23) / 24;  // ~24 anchor rows per segment (geometry only)
+      a.seg_rows = (pl.gh + sseg - 1) / sseg;
+      sseg = (pl.gh + a.seg_rows - 1) / a.seg_rows;
+      if (sseg > 65535) return SSK_E_ARG;
+      pl.grid = dim3(sx, sseg, (p->n + 1) / 2);
+      pl.nparts_per_frame = (size_t)sx * sseg;
+    }
     return SSK_OK;
   }
 
@@ -361,6 +385,11 @@ int run_plan(Plan& pl, double* partials, void* maps, long long* wsums, cudaStrea
     pl.gg.maps = maps;
     return launch_gauss_generic(pl.gg, pl.grid, st);
   }
+  if (pl.strided) {
+    pl.ga.partials = partials;
+    pl.ga.maps = nullptr;
+    return launch_gauss_stride(pl.ga, pl.grid, pl.ga.h - pl.ga.ho + 1, st);
+  }
   if (pl.gauss) {
     pl.ga.partials = partials;
     pl.ga.maps = maps;
@@ -441,11 +470,12 @@ const char* ssk_strerror(int code) {
 
 size_t ssk_ssim_workspace_bytes(const ssk_planes* p, const ssk_window* win) {
   // enough for any `want`: map launches run on narrower strips (more partials) than
-  // score-only launches, and a Σq² launch (rect only) may pick the per-window kernel
-  // (more partials than the block kernel), so take the largest of the plans
+  // score-only launches, a Σq² launch (rect only) may pick the per-window kernel (more
+  // partials than the block kernel) and fp64 Gaussian maps run the generic kernel's
+  // 64-column tiles, so take the largest of the plans
   size_t bytes = 0;
   for (const int want : {SSK_WANT_Q | SSK_WANT_L | SSK_WANT_CS, SSK_WANT_Q | SSK_MAP_TERMS,
-                         SSK_WANT_Q | SSK_WANT_Q2}) {
+                         SSK_WANT_Q | SSK_WANT_Q2, SSK_WANT_Q | SSK_MAP_TERMS | SSK_MAP_F64}) {
     Plan pl;
     if (plan_ssim(p, win, want, pl)) return 0;
     bytes = std::max(bytes, partial_bytes(pl, p->n) * (pl.gauss ? 1 : 2));  // rect: room for q^2

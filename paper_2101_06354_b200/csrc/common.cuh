@@ -10,6 +10,24 @@ namespace ssk {
 // ---------------------------------------------------------------------------
 // cp.async (LDGSTS) 16-byte staging with zero fill of the bytes past `valid`.
 // ---------------------------------------------------------------------------
+// Synchronisation stress build (-DSSK_SYNC_STRESS, tools/sync_stress.py): at every hand-off
+// point of the barrier / mbarrier rings, one warp in four sleeps a pseudo-random 0-1 us,
+// reshuffling the producer/consumer interleavings; a race shows up as results that are no
+// longer bit-identical to the production build's.  Compiled out otherwise.
+#ifdef SSK_SYNC_STRESS
+__device__ __forceinline__ void ssk_jitter(unsigned site) {
+  unsigned h = (unsigned)clock() ^ (blockIdx.x * 0x9E3779B1u) ^ (blockIdx.y * 0x7FEB352Du) ^
+               ((threadIdx.x >> 5) * 0x85EBCA77u) ^ (site * 0xC2B2AE3Du);
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  if ((h & 3u) == 0u) __nanosleep((h >> 4) & 1023u);
+}
+#define SSK_JITTER(site) ::ssk::ssk_jitter(site)
+#else
+#define SSK_JITTER(site) ((void)0)
+#endif
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int valid_bytes) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),

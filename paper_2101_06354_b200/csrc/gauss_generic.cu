@@ -6,6 +6,8 @@
 //   stats_from_sums(area = 1)   (src/stats.py:185-202)
 //   term_maps_from_stats        (src/ssim.py:31-46) and the mean pooling (src/ssim.py:55-65)
 //
+// Also the map API's kernel for every Gaussian window (SSK_MAP_F64: ssim_map and
+// local_statistics return the reference's float64 maps, so they are computed in fp64).
 // Wide windows are rare (the paper's and the reference's default is sigma 1.5 -> 11 taps),
 // so this kernel is generic in K instead of templated: taps live in shared memory and the
 // whole computation runs in fp64 -- the reference's own precision, so no shift or
@@ -69,6 +71,7 @@ __global__ void __launch_bounds__(GG_THREADS) gauss_generic_kernel(const __grid_
 
   for (int r0 = y_begin; r0 < y_end; r0 += GG_TH) {
     // ---- V pass ----
+    SSK_JITTER(400);
     for (int c = tid; c < twc; c += GG_THREADS) {
       const int gc = x0 + c;
       double acc[5][GG_TH];
@@ -105,6 +108,7 @@ __global__ void __launch_bounds__(GG_THREADS) gauss_generic_kernel(const __grid_
         for (int r = 0; r < GG_TH; ++r) s_v[(m * GG_TH + r) * twc + c] = acc[m][r];
     }
     __syncthreads();
+    SSK_JITTER(401);
     // ---- H pass + epilogue ----
     for (int o = tid; o < GG_TH * GG_TW; o += GG_THREADS) {
       const int r = o / GG_TW, j = o % GG_TW;
@@ -133,18 +137,12 @@ __global__ void __launch_bounds__(GG_THREADS) gauss_generic_kernel(const __grid_
       sl += l;
       scs += cs;
       if (terms || stats) {
-        const long long idx = (long long)(orow / a.stride) * a.gw + ocol / a.stride;
-        float* mp = reinterpret_cast<float*>(a.maps) + (long long)frame * a.map_frame + idx;
-        if (terms) {
-          mp[0] = (float)l;
-          mp[a.map_plane] = (float)cs;
-          mp[2 * a.map_plane] = (float)q;
-        } else {
-          mp[0] = (float)mu1;
-          mp[a.map_plane] = (float)mu2;
-          mp[2 * a.map_plane] = (float)var1;
-          mp[3 * a.map_plane] = (float)var2;
-          mp[4 * a.map_plane] = (float)cov;
+        const long long idx = (long long)frame * a.map_frame + (long long)(orow / a.stride) * a.gw + ocol / a.stride;
+        const double vals[5] = {terms ? l : mu1, terms ? cs : mu2, terms ? q : var1, var2, cov};
+        const int np = terms ? 3 : 5;
+        for (int pl = 0; pl < np; ++pl) {
+          if (a.map_f64) reinterpret_cast<double*>(a.maps)[idx + pl * a.map_plane] = vals[pl];
+          else reinterpret_cast<float*>(a.maps)[idx + pl * a.map_plane] = (float)vals[pl];
         }
       }
     }

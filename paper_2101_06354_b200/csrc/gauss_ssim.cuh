@@ -36,6 +36,7 @@
 // (tests/test_stats.py:274-285).
 #pragma once
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -150,9 +151,12 @@ __device__ __forceinline__ u64 sumsq2(u64 x, u64 y) {
 // buffered V tile, synchronised by named barriers, so the two phases overlap
 // instead of alternating behind CTA-wide barriers.
 __device__ __forceinline__ void named_sync(int id, int count) {
+  SSK_JITTER(2 * id);
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+  SSK_JITTER(2 * id + 1);
 }
 __device__ __forceinline__ void named_arrive(int id, int count) {
+  SSK_JITTER(64 + id);
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
@@ -361,6 +365,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
 
   // ---------------- V pass: thread = input column ----------------
   auto vpass = [&](const int c, unsigned char* vbuf) {
+    SSK_JITTER(100);
     if (tid < TWI && c0 + tid < a.w) {
       u64 acc[NM][G];
 #pragma unroll
@@ -462,6 +467,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
 
   // ---------------- H pass + epilogue: thread = (row, 8 columns) ----------------
   auto hpass = [&](const int c, const unsigned char* vbuf) {
+    SSK_JITTER(101);
     const int orow = y0 + c * G + hg;
     const int ocol0 = c0 + 8 * hj;
     if (8 * hj < TW && ocol0 < wo && orow < y1 && (s == 1 || orow % s == 0)) {
@@ -764,7 +770,12 @@ int launch_ws(const GaussArgs& a, dim3 grid, cudaStream_t st) {
       auto fp = gauss_ws_persist_kernel<K, TIN, NM, VC>;
       if (cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return SSK_E_CUDA;
-      const int nctas = (int)std::min<long long>(ntiles, (long long)sm_count());
+      int nctas = (int)std::min<long long>(ntiles, (long long)sm_count());
+      static const int forced = [] {  // SSK_PERSIST_CTAS: fewer CTAs, more tiles each (stress tests)
+        const char* e = std::getenv("SSK_PERSIST_CTAS");
+        return e ? std::atoi(e) : 0;
+      }();
+      if (forced > 0) nctas = (int)std::min<long long>(ntiles, (long long)forced);
       fp<<<nctas, 2 * VC, smem, st>>>(a, (int)grid.x, (int)grid.y);
       note_launch();
       return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;

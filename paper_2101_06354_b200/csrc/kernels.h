@@ -59,6 +59,11 @@ int launch_gauss_u16(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 int launch_gauss_u32(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 int launch_gauss_f32(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 
+// ---------------- K1s: strided Gaussian scores (stride >= 2, 8/16-bit, k <= 31) ----------------
+bool gauss_stride_supported(int dtype, int k, int s);
+int gauss_stride_twa(int k, int s, int es);  // anchor columns per strip
+int launch_gauss_stride(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
+
 // ---------------- K1g: Gaussian windows wider than 31 taps (fp64, generic K) ----------------
 struct GaussGenericArgs {
   const unsigned char* ref;
@@ -72,7 +77,8 @@ struct GaussGenericArgs {
   double c1, c2;
   int want;
   double* partials;            // [n][gridDim.y][gridDim.x][3]
-  void* maps;                  // float32 [n][planes][gh][gw]
+  void* maps;                  // [n][planes][gh][gw], float64 if map_f64 else float32
+  int map_f64;
   long long map_plane, map_frame;
   double taps[255];            // normalised 1-D taps g/sum(g), built in fp64 from sigma
 };

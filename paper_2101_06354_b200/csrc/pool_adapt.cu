@@ -400,7 +400,9 @@ __global__ void __launch_bounds__(PL_THREADS) select_pick_kernel(const __grid_co
     // every thread reads the residual rank before the barrier: the owning thread
     // rewrites st[1] below, and no other thread may see the new value
     const unsigned long long k = st[1];
+    SSK_JITTER(300);
     __syncthreads();
+    SSK_JITTER(301);
     unsigned long long base = 0;
     for (int wi = 0; wi < warp; ++wi) base += wtot[wi];
     const unsigned long long excl = base + incl - s;

@@ -151,7 +151,8 @@ def ssim(pair: DevicePair, window, c1: float, c2: float, want: int, stream=None)
     Returns (sums [n,3] float64 device tensor (sum q, sum l, sum cs; a 4th column sum q^2
     with SSK_WANT_Q2), maps or None).
     Maps: SSK_MAP_TERMS -> [n,3,gh,gw] (l, cs, q); SSK_MAP_STATS -> [n,5,gh,gw];
-    float32 for Gaussian windows, float64 for rect windows.
+    float32 for Gaussian windows (float64 with SSK_MAP_F64: the fp64 kernel), float64 for
+    rect windows.
     """
     torch = nat.torch_mod()
     lib = nat.lib()
@@ -164,7 +165,7 @@ def ssim(pair: DevicePair, window, c1: float, c2: float, want: int, stream=None)
     if want & (nat.MAP_TERMS | nat.MAP_STATS):
         gh, gw = grid_shape(h, w, window.k, window.stride)
         nplanes = 5 if want & nat.MAP_STATS else 3
-        mdt = torch.float32 if window.shape == "gauss" else torch.float64
+        mdt = torch.float32 if window.shape == "gauss" and not want & nat.MAP_F64 else torch.float64
         maps = torch.empty((n, nplanes, gh, gw), dtype=mdt, device=dev)
     ws_bytes = lib.ssk_ssim_workspace_bytes(ctypes.byref(planes), ctypes.byref(win))
     if ws_bytes == 0:

@@ -116,3 +116,14 @@ class UnsupportedMaxval(SsimkitError):
 
 class LengthMismatch(SsimkitError):
     """Paired sequences differ in length."""
+
+
+# The two classes below belong to reference subsystems outside the hot path (the scaled-SSIM
+# histogram matcher, the evaluation harness: SURVEY.md §8 OUT); they complete the exception
+# hierarchy (src/errors.py:113-128) so code catching them still imports.
+class NoReferenceYet(SsimkitError):
+    """Histogram matcher was asked to predict before any reference map."""
+
+
+class TooFew(SsimkitError):
+    """Not enough samples for the requested statistic."""

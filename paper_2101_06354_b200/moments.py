@@ -150,7 +150,7 @@ def local_statistics(ref: PlaneLike, dist: PlaneLike, window: WindowSpec, engine
     bd = plane_bit_depth(ref, 8)
     pair = _pair_to_device(ref, dist, bd, _gauss_like(window))
     peak = float((1 << bd) - 1)
-    _, maps = engine_ssim(pair, window, (0.01 * peak) ** 2, (0.03 * peak) ** 2, nat.MAP_STATS)
+    _, maps = engine_ssim(pair, window, (0.01 * peak) ** 2, (0.03 * peak) ** 2, nat.MAP_STATS | nat.MAP_F64)
     m = maps[0].double().cpu().numpy()
     return LocalStatsMaps(mu1=m[0], mu2=m[1], var1=m[2], var2=m[3], cov=m[4], window_size=window.k,
                           stride=window.stride, source_dims=(h, w))

@@ -58,8 +58,9 @@ def term_maps_from_stats(stats: LocalStatsMaps, c1: float, c2: float) -> SsimTer
 def ssim_map(ref: PlaneLike, dist: PlaneLike, config: SsimConfig = SsimConfig()) -> SsimTermMaps:
     """SSIM term maps of a pair (src/ssim.py:49-52)."""
     pair, dims = _prepare(ref, dist, config)
+    # Gaussian maps from the fp64 kernel (the reference's precision); rect maps are exact anyway
     _, maps = engine.ssim(pair, config.window, config.c1, config.c2,
-                          nat.WANT_Q | nat.WANT_L | nat.WANT_CS | nat.MAP_TERMS)
+                          nat.WANT_Q | nat.WANT_L | nat.WANT_CS | nat.MAP_TERMS | nat.MAP_F64)
     m = maps[0].double().cpu().numpy()
     geom = dict(stride=config.window.stride, source_dims=dims)
     return SsimTermMaps(QualityMap(m[0], **geom), QualityMap(m[1], **geom), QualityMap(m[2], **geom))

@@ -26,7 +26,7 @@ from .errors import DimensionMismatch, GaussianNotSupported3D, ValidationError
 from .moments import LocalStatsMaps
 from .options import MultiscaleSpec, SsimConfig, WindowSpec
 from .planes import PlaneLike, QualityMap, ScoreSeries, plane_data, validate_frame_pair
-from .pyramid import combine_scale_scores, dyadic_downsample
+from .pyramid import combine_scale_scores, dyadic_downsample, msssim
 from .scoring import SsimTermMaps
 
 REFRESH_INTERVAL = 300
@@ -305,6 +305,8 @@ def msssim3d(ref_frames: Iterable[PlaneLike], dist_frames: Iterable[PlaneLike], 
     spec = MultiscaleSpec.product() if spec is None else spec
     if not spec.enabled:
         raise ValidationError("multiscale aggregation is off; use ssim3d_series instead")
+    if kt == 1 and config.window.shape == "rect":  # one-frame volume = the 2-D window: framewise MS-SSIM
+        return ScoreSeries(np.asarray([msssim(r, d, config, spec) for r, d in zip(ref_frames, dist_frames)]))
     volumes = [RollingVolume(kt) for _ in range(spec.levels)]
     scores = []
     for ref, dist in zip(ref_frames, dist_frames):

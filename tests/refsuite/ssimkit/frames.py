@@ -1,0 +1,6 @@
+"""Alias of the reference's ssimkit.frames onto the B200 engine (see __init__.py)."""
+from . import lookup
+
+
+def __getattr__(name):
+    return lookup("frames", name)

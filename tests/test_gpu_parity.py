@@ -930,3 +930,81 @@ def test_score_only_bright_middle_row_over_dark(cuda, oracle):
     assert max(abs(x - y) for x, y in zip(terms, want)) < SCORE_TOL
     q = P.ssim_map(a, b, cfg).q_map.values
     assert abs(float(q.mean()) - terms[0]) < SCORE_TOL
+
+
+@pytest.mark.parametrize("k,sigma,s,kind,h,w", [
+    (11, 1.5, 2, "u8", 131, 517), (11, 1.5, 5, "u8", 300, 700), (11, 1.5, 3, "u16", 97, 260),
+    (7, 1.0, 8, "u8", 120, 333), (31, 5.0, 4, "u8", 150, 600), (11, 1.5, 13, "u8", 90, 400),
+    (3, 0.5, 2, "u16", 40, 300), (11, 1.5, 5, "u16", 1080, 1920),
+])
+def test_strided_gaussian_scores_vs_oracle(cuda, oracle, k, sigma, s, kind, h, w):
+    """Strided Gaussian score launches run the anchor-only kernel (K1s): SSIM terms of an odd
+    batch (a lone frame in the last packed pair) within 1e-5 of the float64 oracle, strides
+    below, equal to and above k, 8- and 16-bit samples, strips and segments with ragged edges;
+    MS-SSIM with a strided window at every level too."""
+    import torch
+    from paper_2101_06354_b200 import synth
+
+    rng = np.random.default_rng(k * 1000 + s * 10 + h)
+    bd = 8 if kind == "u8" else 10
+    peak = (1 << bd) - 1
+    dt = np.uint8 if kind == "u8" else np.uint16
+    frames = []
+    for _ in range(3):
+        a = synth.inv_f_noise(rng, h, w, float(peak))
+        b = np.clip(np.round(a + rng.normal(0, peak / 30.0, a.shape)), 0, peak)
+        frames.append((a.astype(dt), b.astype(dt)))
+    cfg = P.SsimConfig(bit_depth=bd, window=P.WindowSpec.gaussian(sigma, k=k, stride=s))
+    ref = torch.from_numpy(np.stack([f[0] for f in frames])).to(cuda)
+    dist = torch.from_numpy(np.stack([f[1] for f in frames])).to(cuda)
+    t = P.ssim_terms_batch(ref, dist, cfg)
+    got = np.stack([t.score.cpu().numpy(), t.l_mean.cpu().numpy(), t.cs_mean.cpu().numpy()], axis=1)
+    win = dict(shape="gauss", k=k, sigma=sigma, stride=s, bit_depth=bd)
+    for i, (a, b) in enumerate(frames):
+        assert np.max(np.abs(got[i] - np.array(oracle.ssim_terms(a, b, **win)))) < SCORE_TOL, i
+    if min(h, w) // 4 >= k:
+        ms = P.msssim_batch(ref, dist, cfg, P.MultiscaleSpec.product(3)).cpu().numpy()
+        for i, (a, b) in enumerate(frames):
+            assert abs(ms[i] - oracle.msssim(a, b, 3, **win)) < SCORE_TOL, i
+    # the map path (K1, anchor masking) agrees with the anchor-only scores
+    q = P.ssim_map(P.LumaPlane(frames[0][0], bd), P.LumaPlane(frames[0][1], bd), cfg).q_map.values
+    assert abs(float(q.mean()) - got[0, 0]) < SCORE_TOL
+
+
+@pytest.mark.parametrize("name", ["gauss11", "gauss_s3", "gauss13_10b"])
+def test_gaussian_map_api_is_fp64(cuda, golden, name):
+    """ssim_map / local_statistics (the reference's map API) compute Gaussian maps with the
+    fp64 kernel (SSK_MAP_F64): within 1e-12 of the reference's float64 maps, not just 1e-4."""
+    cfg, bd, _ = CASES[name]
+    ra, rb = planes(golden, name, bd)
+    maps = P.ssim_map(ra, rb, cfg)
+    for key, got in (("l", maps.l_map.values), ("cs", maps.cs_map.values), ("q", maps.q_map.values)):
+        assert got.dtype == np.float64
+        assert np.max(np.abs(got - golden[f"{name}/{key}"])) < 1e-12
+    st = P.local_statistics(ra, rb, cfg.window, cfg.engine)
+    want = golden[f"{name}/stats"]
+    scale = float((1 << bd) - 1) ** 2
+    for i, got in enumerate((st.mu1, st.mu2, st.var1, st.var2, st.cov)):
+        assert np.max(np.abs(got - want[i])) < 1e-12 * scale
+
+
+@pytest.mark.parametrize("bar", [20, 150])
+def test_fp32_map_kernel_letterbox_vs_oracle(cuda, oracle, bar):
+    """The fp32 K1 map launches (used inside batch pooling; per-chunk sample shift) on dark
+    letterbox bars: maps within 1e-4 of the float64 oracle."""
+    import torch
+    from paper_2101_06354_b200 import _native as nat
+    from paper_2101_06354_b200 import synth
+
+    rng = np.random.default_rng(bar + 1)
+    a = synth.inv_f_noise(rng, 300, 520, 255.0).astype(np.uint8)
+    a[:bar] = rng.integers(0, 3, (bar, 520))
+    b = np.clip(a.astype(int) + rng.integers(-1, 2, a.shape), 0, 255).astype(np.uint8)
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    pair = engine.device_pair(torch.from_numpy(a[None]).cuda(), torch.from_numpy(b[None]).cuda(), 8, gauss=True)
+    _, maps = engine.ssim(pair, cfg.window, cfg.c1, cfg.c2, nat.WANT_Q | nat.MAP_TERMS)
+    assert maps.dtype == torch.float32
+    m = maps[0].double().cpu().numpy()
+    wl, wcs, wq = oracle.ssim_maps(a, b, shape="gauss", k=11, sigma=1.5)
+    for g, w_ in zip(m, (wl, wcs, wq)):
+        assert np.max(np.abs(g - w_)) < MAP_TOL

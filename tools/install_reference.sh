@@ -13,4 +13,7 @@ rm -rf "$REPO/baseline/_ref"
 python -m pip install --no-index --no-build-isolation --no-deps --find-links /opt/wheelhouse \
     --target "$REPO/baseline/_ref" "$TMP/pkg"
 rm -rf "$TMP"
+# the reference's own test files, run against the engine by tests/test_gpu_reference_suite.py
+# (through the ssimkit alias in tests/refsuite; they stay untracked like the package itself)
+cp -r "$SRC/tests" "$REPO/baseline/_ref/ssimkit_tests"
 python -c "import sys; sys.path.insert(0, '$REPO/baseline/_ref'); import ssimkit; print('ssimkit', ssimkit.__file__)"

@@ -1,0 +1,137 @@
+"""Synchronisation stress test: the evidence for race freedom on a pool without compute-sanitizer.
+
+compute-sanitizer is closed on this GPU pool, so races are hunted by perturbation instead:
+
+  1. the production library computes every case below once (the expected outputs);
+  2. the stress build (``python -m paper_2101_06354_b200.csrc.build --stress``: the same
+     sources with -DSSK_SYNC_STRESS, where one warp in four sleeps a pseudo-random 0-1 us
+     at every barrier / mbarrier hand-off -- named-barrier V-tile ring of K1, cp.async raw
+     ring, persistent tile walk, cp.async.bulk + mbarrier ring of the box kernel, radix
+     select, generic kernel) recomputes them several times, and with the persistent K1
+     forced onto 1, 3 and 37 CTAs (SSK_PERSIST_CTAS: every CTA walks many tiles, so the
+     V-tile ring and its barrier phases run on across tile boundaries);
+  3. every output must be BIT-identical to step 1 (all reductions here have a fixed
+     order, so any difference is a race or an uninitialised read).
+
+    python tools/sync_stress.py            # prints one JSON summary line; exit 1 on mismatch
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+import tempfile
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parents[1]
+STRESS_LIB = REPO / "paper_2101_06354_b200" / "_lib" / "stress" / "libssimk.so"
+
+
+def run_cases(out_path: str) -> None:
+    sys.path.insert(0, str(REPO))
+    import numpy as np
+    import torch
+
+    import paper_2101_06354_b200 as P
+    from paper_2101_06354_b200 import synth
+
+    rng = np.random.default_rng(11)
+    out: dict[str, np.ndarray] = {}
+
+    def u8(n, h, w):
+        a = rng.integers(0, 256, (n, h, w)).astype(np.uint8)
+        b = np.clip(a.astype(int) + rng.integers(-30, 31, a.shape), 0, 255).astype(np.uint8)
+        return torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+
+    def put(name, *tensors):
+        out[name] = np.concatenate([np.asarray(t.cpu() if hasattr(t, "cpu") else t, dtype=np.float64).ravel()
+                                    for t in tensors])
+
+    g = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    # persistent wide K1 (252 tiles), with and without the fused level-1 stores
+    a, b = u8(41, 512, 600)
+    t = P.ssim_terms_batch(a, b, g)
+    put("persist_terms", t.score, t.l_mean, t.cs_mean)
+    put("persist_msssim", P.msssim_batch(a[:9], b[:9], g, P.MultiscaleSpec.product(3)))
+    # coarse levels (u16 / u32), pyramid, 5-scale MS-SSIM; config-2 size
+    a, b = u8(4, 1080, 1920)
+    ms, t = P.msssim_batch(a, b, g, P.MultiscaleSpec.product(5), with_ssim=True)
+    put("levels_1080p", ms, t.score, t.l_mean, t.cs_mean)
+    xn = rng.integers(0, 1024, (2, 480, 704)).astype(np.uint16)
+    x = torch.from_numpy(xn).cuda()
+    y = torch.from_numpy(np.minimum(xn + 3, 1023).astype(np.uint16)).cuda()
+    put("levels_10bit", P.msssim_batch(x, y,
+                                       P.SsimConfig(bit_depth=10, window=P.WindowSpec.gaussian(1.5)),
+                                       P.MultiscaleSpec.product(5)))
+    # classic K1 map launches (per-chunk shift), statistics maps
+    a, b = u8(1, 300, 520)
+    an, bn = a[0].cpu().numpy(), b[0].cpu().numpy()
+    m = P.ssim_map(an, bn, g)
+    put("maps_terms", m.l_map.values, m.cs_map.values, m.q_map.values)
+    st = P.local_statistics(an, bn, P.WindowSpec.gaussian(1.5))
+    put("maps_stats", st.mu1, st.mu2, st.var1, st.var2, st.cov)
+    # box kernels: bulk-copy block kernel (config-4 crop), running-sum kernel with q^2 (cov pooling)
+    ra, rb = synth.config4_pair(0, 512, 1024)
+    ta, tb = torch.from_numpy(np.stack([ra, rb])).cuda(), torch.from_numpy(np.stack([rb, ra])).cuda()
+    t = P.ssim_terms_batch(ta, tb, P.SsimConfig(bit_depth=10, window=P.WindowSpec.rectangular(8, stride=4),
+                                                engine="integral"))
+    put("box_block", t.score, t.l_mean, t.cs_mean)
+    rec = P.score_frame_pair(P.LumaPlane(ra, 10), P.LumaPlane(rb, 10),
+                             P.SsimConfig(bit_depth=10, window=P.WindowSpec.rectangular(11, stride=5),
+                                          spatial_pool="cov"))
+    put("box_int_cov", [rec.score, rec.am])
+    # generic (k > 31) kernel
+    a, b = u8(2, 150, 230)
+    t = P.ssim_terms_batch(a, b, P.SsimConfig(window=P.WindowSpec.gaussian(6.0)))
+    put("generic", t.score, t.l_mean, t.cs_mean)
+    # radix select (fns / median) and the CoV sums
+    q = 1.0 - 0.05 * torch.rand((3, 200, 300), dtype=torch.float32, device="cuda",
+                                generator=torch.Generator("cuda").manual_seed(5)) ** 3
+    for meth in ("fns", "pp:6,4000", "cov"):
+        pooled, mean = P.pool_maps(q, meth)
+        put(f"pool_{meth.split(':')[0]}", pooled, mean)
+    torch.cuda.synchronize()
+    np.savez(out_path, **out)
+
+
+def main() -> int:
+    if len(sys.argv) > 2 and sys.argv[1] == "--cases":
+        run_cases(sys.argv[2])
+        return 0
+    import numpy as np
+
+    if not STRESS_LIB.exists():
+        sys.path.insert(0, str(REPO))
+        from paper_2101_06354_b200.csrc import build
+
+        build.build(stress=True)
+    runs = [("production", {}), ("stress", {}), ("stress", {}), ("stress", {"SSK_PERSIST_CTAS": "1"}),
+            ("stress", {"SSK_PERSIST_CTAS": "3"}), ("stress", {"SSK_PERSIST_CTAS": "37"}), ("stress", {})]
+    results = []
+    with tempfile.TemporaryDirectory() as td:
+        for i, (lib, extra) in enumerate(runs):
+            env = dict(os.environ, **extra)
+            if lib == "stress":
+                env["SSK_LIBRARY"] = str(STRESS_LIB)
+            path = os.path.join(td, f"run{i}.npz")
+            r = subprocess.run([sys.executable, __file__, "--cases", path], env=env, capture_output=True, text=True)
+            if r.returncode != 0:
+                print(r.stderr[-3000:], file=sys.stderr)
+                return 2
+            with np.load(path) as z:
+                results.append({k: z[k] for k in z.files})
+    base = results[0]
+    mismatches = []
+    for i, res in enumerate(results[1:], 1):
+        for k, v in base.items():
+            if not np.array_equal(v, res[k], equal_nan=True):
+                mismatches.append({"run": i, "env": runs[i][1], "case": k,
+                                   "max_abs": float(np.nanmax(np.abs(v - res[k])))})
+    print(json.dumps({"tool": "sync_stress", "cases": sorted(base), "runs": [dict(lib=l, **e) for l, e in runs],
+                      "outputs_compared": len(base) * (len(results) - 1), "mismatches": mismatches}))
+    return 1 if mismatches else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
