@@ -336,6 +336,18 @@ int ssk_delta_e(const ssk_color* ref, const ssk_color* dist, int smooth, int k, 
 int ssk_host_register(void* ptr, size_t bytes, int read_only);
 int ssk_host_unregister(void* ptr);
 
+/* Elementwise fp64 map arithmetic of the public API, in the reference's operation order
+ * (bit-identical to numpy on the same inputs).  Device pointers, `count` elements each:
+ *   ssk_stats_from_sums: stats_from_sums (src/stats.py:185-202); d_out [5][count] =
+ *     mu1, mu2, var1, var2 (clamped at 0), cov (not clamped), from window sums over `area`;
+ *   ssk_term_maps: term_maps_from_stats (src/ssim.py:31-46); d_out [3][count] = l, cs, q;
+ *   ssk_divide: d_out[i] = d_x[i] / divisor (IEEE division: per-frame means from sums). */
+int ssk_stats_from_sums(const double* d_s1, const double* d_s2, const double* d_q1, const double* d_q2,
+                        const double* d_p12, int64_t count, double area, double* d_out, void* stream);
+int ssk_term_maps(const double* d_mu1, const double* d_mu2, const double* d_var1, const double* d_var2,
+                  const double* d_cov, int64_t count, double c1, double c2, double* d_out, void* stream);
+int ssk_divide(const double* d_x, int64_t count, double divisor, double* d_out, void* stream);
+
 /* Number of kernels this library has launched since load (for bench.py). */
 uint64_t ssk_launch_count(void);
 

@@ -39,6 +39,9 @@ GAUSS_MAX_K = 255  # SSK_GAUSS_MAX_K
 
 EXPORTED_SYMBOLS = (
     "ssk_abi_version",
+    "ssk_stats_from_sums",
+    "ssk_term_maps",
+    "ssk_divide",
     "ssk_strerror",
     "ssk_ssim_workspace_bytes",
     "ssk_msssim_workspace_bytes",
@@ -179,6 +182,12 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         lib.ssk_ssim_workspace_bytes.argtypes = [pP, pW]
         lib.ssk_msssim_workspace_bytes.restype = sz
         lib.ssk_msssim_workspace_bytes.argtypes = [pP, pW, i32]
+        lib.ssk_stats_from_sums.restype = i32
+        lib.ssk_stats_from_sums.argtypes = [vp, vp, vp, vp, vp, i64, ctypes.c_double, vp, vp]
+        lib.ssk_term_maps.restype = i32
+        lib.ssk_term_maps.argtypes = [vp, vp, vp, vp, vp, i64, ctypes.c_double, ctypes.c_double, vp, vp]
+        lib.ssk_divide.restype = i32
+        lib.ssk_divide.argtypes = [vp, i64, ctypes.c_double, vp, vp]
         lib.ssk_ssim.restype = i32
         lib.ssk_ssim.argtypes = [pP, pW, i32, vp, vp, vp, sz, vp]
         lib.ssk_box_window_sums.restype = i32

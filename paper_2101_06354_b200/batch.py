@@ -45,7 +45,7 @@ def ssim_terms_batch(ref, dist, config: SsimConfig = SsimConfig(), stream=None) 
     sums, _ = engine.ssim(pair, config.window, config.c1, config.c2,
                           nat.WANT_Q | nat.WANT_L | nat.WANT_CS, stream)
     gh, gw = engine.grid_shape(h, w, config.window.k, config.window.stride)
-    means = engine.frame_means(sums, gh * gw)
+    means = engine.frame_means(sums, gh * gw, stream)
     return FrameTerms(means[:, 0], means[:, 1], means[:, 2])
 
 

@@ -2,6 +2,8 @@
 // summed-area tables for the IntegralSet API, and the FP32 peak probe.
 #include <type_traits>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -484,6 +486,86 @@ int launch_msssim_finalize(const FinalizeArgs& a, cudaStream_t st) {
   if (a.n < 1) return SSK_OK;
   if (a.levels < 1 || a.levels > SSK_MAX_SCALES) return SSK_E_ARG;
   msssim_finalize_kernel<<<a.n, 32 * (a.levels + 3), 0, st>>>(a);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+}
+
+}  // namespace ssk
+
+// ---------------------------------------------------------------------------
+// Elementwise map arithmetic of the public API (off the throughput path, where it is
+// fused into K1 / K2): stats_from_sums (src/stats.py:185-202), term_maps_from_stats
+// (src/ssim.py:31-46) and the per-frame means.  fp64 with IEEE-rounded intrinsics in the
+// reference's operation order (no FMA contraction), so the results are bit-identical to
+// numpy's evaluation of the same expressions.
+// ---------------------------------------------------------------------------
+namespace ssk {
+namespace {
+
+__global__ void stats_from_sums_kernel(const double* __restrict__ s1, const double* __restrict__ s2,
+                                       const double* __restrict__ q1, const double* __restrict__ q2,
+                                       const double* __restrict__ p12, long long count, double area,
+                                       double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double mu1 = __ddiv_rn(s1[i], area), mu2 = __ddiv_rn(s2[i], area);
+    out[i] = mu1;
+    out[count + i] = mu2;
+    out[2 * count + i] = fmax(__dsub_rn(__ddiv_rn(q1[i], area), __dmul_rn(mu1, mu1)), 0.0);
+    out[3 * count + i] = fmax(__dsub_rn(__ddiv_rn(q2[i], area), __dmul_rn(mu2, mu2)), 0.0);
+    out[4 * count + i] = __dsub_rn(__ddiv_rn(p12[i], area), __dmul_rn(mu1, mu2));
+  }
+}
+
+__global__ void term_maps_kernel(const double* __restrict__ mu1, const double* __restrict__ mu2,
+                                 const double* __restrict__ var1, const double* __restrict__ var2,
+                                 const double* __restrict__ cov, long long count, double c1, double c2,
+                                 double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double m1 = mu1[i], m2 = mu2[i];
+    // l = (2.0 * mu1 * mu2 + c1) / (mu1 * mu1 + mu2 * mu2 + c1), numpy's left-to-right order
+    const double l = __ddiv_rn(__dadd_rn(__dmul_rn(__dmul_rn(2.0, m1), m2), c1),
+                               __dadd_rn(__dadd_rn(__dmul_rn(m1, m1), __dmul_rn(m2, m2)), c1));
+    const double cs = __ddiv_rn(__dadd_rn(__dmul_rn(2.0, cov[i]), c2), __dadd_rn(__dadd_rn(var1[i], var2[i]), c2));
+    out[i] = l;
+    out[count + i] = cs;
+    out[2 * count + i] = __dmul_rn(l, cs);
+  }
+}
+
+__global__ void divide_kernel(const double* __restrict__ x, long long count, double divisor, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = __ddiv_rn(x[i], divisor);
+}
+
+dim3 ew_grid(long long count) {
+  long long b = (count + 255) / 256;
+  return dim3((unsigned)std::max(1LL, std::min(b, 148LL * 16)));
+}
+
+}  // namespace
+
+int launch_stats_from_sums(const double* s1, const double* s2, const double* q1, const double* q2,
+                           const double* p12, long long count, double area, double* out, cudaStream_t st) {
+  if (count < 1) return SSK_OK;
+  stats_from_sums_kernel<<<ew_grid(count), 256, 0, st>>>(s1, s2, q1, q2, p12, count, area, out);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+}
+
+int launch_term_maps(const double* mu1, const double* mu2, const double* var1, const double* var2,
+                     const double* cov, long long count, double c1, double c2, double* out, cudaStream_t st) {
+  if (count < 1) return SSK_OK;
+  term_maps_kernel<<<ew_grid(count), 256, 0, st>>>(mu1, mu2, var1, var2, cov, count, c1, c2, out);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
+}
+
+int launch_divide(const double* x, long long count, double divisor, double* out, cudaStream_t st) {
+  if (count < 1) return SSK_OK;
+  divide_kernel<<<ew_grid(count), 256, 0, st>>>(x, count, divisor, out);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? SSK_OK : SSK_E_CUDA;
 }

@@ -813,6 +813,25 @@ int ssk_volume_ssim(const ssk_volume* v, const ssk_window* win, int want, double
   return launch_reduce_partials(partials, (int)pl.nparts_per_frame, 1, 3, 1.0, d_sums, 3, 0, 0, st);
 }
 
+int ssk_stats_from_sums(const double* d_s1, const double* d_s2, const double* d_q1, const double* d_q2,
+                        const double* d_p12, int64_t count, double area, double* d_out, void* stream) {
+  if (!d_s1 || !d_s2 || !d_q1 || !d_q2 || !d_p12 || !d_out || count < 0 || !(area > 0.0)) return SSK_E_ARG;
+  return launch_stats_from_sums(d_s1, d_s2, d_q1, d_q2, d_p12, count, area, d_out,
+                                static_cast<cudaStream_t>(stream));
+}
+
+int ssk_term_maps(const double* d_mu1, const double* d_mu2, const double* d_var1, const double* d_var2,
+                  const double* d_cov, int64_t count, double c1, double c2, double* d_out, void* stream) {
+  if (!d_mu1 || !d_mu2 || !d_var1 || !d_var2 || !d_cov || !d_out || count < 0) return SSK_E_ARG;
+  return launch_term_maps(d_mu1, d_mu2, d_var1, d_var2, d_cov, count, c1, c2, d_out,
+                          static_cast<cudaStream_t>(stream));
+}
+
+int ssk_divide(const double* d_x, int64_t count, double divisor, double* d_out, void* stream) {
+  if (!d_x || !d_out || count < 0) return SSK_E_ARG;
+  return launch_divide(d_x, count, divisor, d_out, static_cast<cudaStream_t>(stream));
+}
+
 uint64_t ssk_launch_count(void) { return g_launches.load(); }
 
 int ssk_host_register(void* ptr, size_t bytes, int read_only) {

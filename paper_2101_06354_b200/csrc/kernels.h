@@ -59,6 +59,13 @@ int launch_gauss_u16(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 int launch_gauss_u32(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 int launch_gauss_f32(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 
+// ---------------- elementwise map arithmetic of the public API (aux_kernels.cu) ----------------
+int launch_stats_from_sums(const double* s1, const double* s2, const double* q1, const double* q2,
+                           const double* p12, long long count, double area, double* out, cudaStream_t st);
+int launch_term_maps(const double* mu1, const double* mu2, const double* var1, const double* var2,
+                     const double* cov, long long count, double c1, double c2, double* out, cudaStream_t st);
+int launch_divide(const double* x, long long count, double divisor, double* out, cudaStream_t st);
+
 // ---------------- K1s: strided Gaussian scores (stride >= 2, 8/16-bit, k <= 31) ----------------
 bool gauss_stride_supported(int dtype, int k, int s);
 int gauss_stride_twa(int k, int s, int es);  // anchor columns per strip

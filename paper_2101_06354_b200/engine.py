@@ -46,6 +46,8 @@ def _classify(a: np.ndarray, want_gauss: bool) -> tuple[np.dtype, int]:
     """Storage dtype + C-ABI code for a host sample array."""
     if a.dtype == np.uint8:
         return np.dtype(np.uint8), nat.U8
+    if a.dtype == np.uint16:  # fits u16 by type: no range scan
+        return np.dtype(np.uint16), nat.U16
     if a.dtype.kind in "ui":
         lo, hi = int(a.min()), int(a.max())
         if lo >= 0 and hi <= 255 and a.dtype.itemsize == 1:
@@ -69,8 +71,11 @@ def _effective_depth(arrs, code: int, bit_depth: int) -> int:
 
 
 def upload_pair(ref: np.ndarray, dist: np.ndarray, bit_depth: int, gauss: bool,
-                device=None, stream=None) -> DevicePair:
-    """Copy one or a batch of host frame pairs into aligned device buffers."""
+                device=None, stream=None, validated: bool = False) -> DevicePair:
+    """Copy one or a batch of host frame pairs into aligned device buffers (on ``stream``, or
+    the current stream).  ``validated``: the samples already passed the container range
+    check (``LumaPlane``: integers in [0, 2^bit_depth - 1]), so ``bit_depth`` bounds them and
+    no host scan is repeated here."""
     torch = nat.torch_mod()
     device = device or nat.require_device()
     a = np.asarray(ref)
@@ -92,10 +97,13 @@ def upload_pair(ref: np.ndarray, dist: np.ndarray, bit_depth: int, gauss: bool,
     hv[1, :, :, :w] = b
     if pitch > w:
         hv[:, :, :, w:] = 0
-    dev = host.to(device, non_blocking=True)
     if stream is not None:
-        pass
-    depth = _effective_depth((a, b), code, bit_depth)
+        with torch.cuda.stream(stream):
+            dev = host.to(device, non_blocking=True)
+    else:
+        dev = host.to(device, non_blocking=True)
+    depth = (max(8, min(16, bit_depth)) if validated and code in (nat.U8, nat.U16)
+             else _effective_depth((a, b), code, bit_depth))
     return DevicePair(dev[0, :, :, :w], dev[1, :, :, :w], code, depth)
 
 
@@ -311,12 +319,15 @@ def to_float64(pair_tensor, code: int, scale_log2: int):
     return v * (2.0 ** -scale_log2) if scale_log2 else v
 
 
-def frame_means(sums, count: int):
-    """sums / count with an IEEE division on the device (a 0-dim CUDA divisor, so torch
-    does not substitute a reciprocal multiply); every path derives means this way,
-    so per-pair and batched scores are bit-identical."""
+def frame_means(sums, count: int, stream=None):
+    """sums / count with an IEEE division on the device (``ssk_divide``); every path derives
+    means this way, so per-pair and batched scores are bit-identical."""
     torch = nat.torch_mod()
-    return sums / torch.full((), float(count), dtype=torch.float64, device=sums.device)
+    src = sums.contiguous()
+    out = torch.empty_like(src)
+    nat.raise_for(nat.lib().ssk_divide(src.data_ptr(), src.numel(), float(count), out.data_ptr(),
+                                       nat.stream_handle(stream)), "frame_means")
+    return out
 
 
 def launch_count() -> int:

@@ -78,7 +78,7 @@ def _gauss_like(window) -> bool:
 
 def _pair_to_device(ref: PlaneLike, dist: PlaneLike, bit_depth: int, gauss: bool):
     a, b = plane_data(ref), plane_data(dist)
-    return engine.upload_pair(a, b, bit_depth, gauss)
+    return engine.upload_pair(a, b, bit_depth, gauss, validated=True)  # callers validated the pair
 
 
 def build_integral_set(ref: PlaneLike, dist: PlaneLike) -> IntegralSet:
@@ -87,7 +87,7 @@ def build_integral_set(ref: PlaneLike, dist: PlaneLike) -> IntegralSet:
     bd = plane_bit_depth(ref, 8)
     a, b = plane_data(ref), plane_data(dist)
     both_int = a.dtype.kind in "uib" and b.dtype.kind in "uib"
-    pair = engine.upload_pair(a, b, bd, gauss=False)
+    pair = engine.upload_pair(a, b, bd, gauss=False, validated=True)
     if both_int and pair.code not in (nat.U8, nat.U16):
         raise ValidationError("integer samples beyond 16 bits are not supported by the integral engine")
     if not both_int and pair.code != nat.F64:
@@ -161,12 +161,19 @@ def engine_ssim(pair, window, c1, c2, want):
 
 
 def stats_from_sums(s1, s2, q1, q2, p12, area: float):
-    """Moments from raw window sums over ``area`` samples (src/stats.py:185-202), float64 on device."""
+    """Moments from raw window sums over ``area`` samples (src/stats.py:185-202): the fp64
+    elementwise kernel ``ssk_stats_from_sums`` (the reference's operation order, bit-identical)."""
     torch = nat.torch_mod()
     dev = nat.require_device()
-    t = [torch.as_tensor(np.asarray(x, dtype=np.float64), device=dev) for x in (s1, s2, q1, q2, p12)]
-    mu1, mu2 = t[0] / area, t[1] / area
-    var1 = torch.clamp_min(t[2] / area - mu1 * mu1, 0.0)
-    var2 = torch.clamp_min(t[3] / area - mu2 * mu2, 0.0)
-    cov = t[4] / area - mu1 * mu2
-    return tuple(x.cpu().numpy() for x in (mu1, mu2, var1, var2, cov))
+    arrs = [np.asarray(x, dtype=np.float64) for x in (s1, s2, q1, q2, p12)]
+    shape = np.broadcast_shapes(*(a.shape for a in arrs))
+    if not float(area) > 0.0:
+        raise ValidationError(f"window area must be positive, got {area!r}")
+    if int(np.prod(shape)) == 0:
+        return tuple(np.zeros(shape) for _ in range(5))
+    t = torch.from_numpy(np.stack([np.broadcast_to(a, shape).ravel() for a in arrs])).to(dev)
+    out = torch.empty((5, t.shape[1]), dtype=torch.float64, device=dev)
+    nat.raise_for(nat.lib().ssk_stats_from_sums(*(t[i].data_ptr() for i in range(5)), t.shape[1], float(area),
+                                                 out.data_ptr(), nat.stream_handle(None)), "stats_from_sums")
+    host = out.cpu().numpy()
+    return tuple(host[i].reshape(shape) for i in range(5))

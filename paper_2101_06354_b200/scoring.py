@@ -37,22 +37,27 @@ def _prepare(ref: PlaneLike, dist: PlaneLike, config: SsimConfig):
     h, w = a.shape
     check_fit(h, w, config.window.k)
     resolve_engine(config.window, config.engine)
-    pair = engine.upload_pair(a, b, plane_bit_depth(ref, config.bit_depth), config.window.shape == "gauss")
+    pair = engine.upload_pair(a, b, plane_bit_depth(ref, config.bit_depth), config.window.shape == "gauss",
+                              validated=True)
     return pair, (h, w)
 
 
 def term_maps_from_stats(stats: LocalStatsMaps, c1: float, c2: float) -> SsimTermMaps:
-    """l, cs, q from given statistics grids (src/ssim.py:31-46), float64 on the device."""
+    """l, cs, q from given statistics grids (src/ssim.py:31-46): the fp64 elementwise kernel
+    ``ssk_term_maps`` (the reference's operation order, bit-identical)."""
     torch = nat.torch_mod()
     dev = nat.require_device()
-    mu1, mu2, var1, var2, cov = (torch.as_tensor(np.asarray(x, dtype=np.float64), device=dev)
-                                 for x in (stats.mu1, stats.mu2, stats.var1, stats.var2, stats.cov))
-    l_map = (2.0 * mu1 * mu2 + c1) / (mu1 * mu1 + mu2 * mu2 + c1)
-    cs_map = (2.0 * cov + c2) / (var1 + var2 + c2)
-    q = l_map * cs_map
+    grids = [np.asarray(x, dtype=np.float64) for x in (stats.mu1, stats.mu2, stats.var1, stats.var2, stats.cov)]
+    shape = grids[0].shape
     geom = dict(stride=stats.stride, source_dims=stats.source_dims)
-    return SsimTermMaps(QualityMap(l_map.cpu().numpy(), **geom), QualityMap(cs_map.cpu().numpy(), **geom),
-                        QualityMap(q.cpu().numpy(), **geom))
+    if grids[0].size == 0:
+        return SsimTermMaps(*(QualityMap(np.zeros(shape), **geom) for _ in range(3)))
+    t = torch.from_numpy(np.stack([g.ravel() for g in grids])).to(dev)
+    out = torch.empty((3, t.shape[1]), dtype=torch.float64, device=dev)
+    nat.raise_for(nat.lib().ssk_term_maps(*(t[i].data_ptr() for i in range(5)), t.shape[1], float(c1), float(c2),
+                                           out.data_ptr(), nat.stream_handle(None)), "term_maps_from_stats")
+    host = out.cpu().numpy()
+    return SsimTermMaps(*(QualityMap(host[i].reshape(shape), **geom) for i in range(3)))
 
 
 def ssim_map(ref: PlaneLike, dist: PlaneLike, config: SsimConfig = SsimConfig()) -> SsimTermMaps:

@@ -1008,3 +1008,27 @@ def test_fp32_map_kernel_letterbox_vs_oracle(cuda, oracle, bar):
     wl, wcs, wq = oracle.ssim_maps(a, b, shape="gauss", k=11, sigma=1.5)
     for g, w_ in zip(m, (wl, wcs, wq)):
         assert np.max(np.abs(g - w_)) < MAP_TOL
+
+
+def test_stats_and_term_maps_api_bit_exact(cuda, oracle, rng):
+    """stats_from_sums / term_maps_from_stats run on the fp64 elementwise kernels in the
+    reference's operation order: bit-identical to numpy's evaluation (oracle), including the
+    variance clamp and broadcasting of a scalar sum."""
+    from paper_2101_06354_b200 import moments, scoring
+
+    shape = (37, 53)
+    s1, s2 = rng.uniform(0, 255 * 121, shape), rng.uniform(0, 255 * 121, shape)
+    q1 = s1 * s1 / 121 + rng.uniform(-5, 500, shape)  # some windows clamp at 0
+    q2, p12 = s2 * s2 / 121 + rng.uniform(0, 500, shape), s1 * s2 / 121 + rng.uniform(-300, 300, shape)
+    got = moments.stats_from_sums(s1, s2, q1, q2, p12, 121.0)
+    want = oracle.moments_from_sums(s1, s2, q1, q2, p12, 121.0)
+    for g, w_ in zip(got, want):
+        assert np.array_equal(g, w_)
+    st = P.LocalStatsMaps(mu1=want[0], mu2=want[1], var1=want[2], var2=want[3], cov=want[4], window_size=11,
+                          stride=1, source_dims=(47, 63))
+    maps = scoring.term_maps_from_stats(st, 6.5025, 58.5225)
+    wl, wcs, wq = oracle.term_maps(*want, 6.5025, 58.5225)
+    assert np.array_equal(maps.l_map.values, wl) and np.array_equal(maps.cs_map.values, wcs)
+    assert np.array_equal(maps.q_map.values, wq)
+    one = moments.stats_from_sums(np.float64(10.0), s2, q1, q2, p12, 121.0)[0]
+    assert one.shape == shape and np.all(one == 10.0 / 121.0)
