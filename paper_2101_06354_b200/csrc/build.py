@@ -40,17 +40,21 @@ def _stale(lib: Path = LIB) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, stress: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, stress: bool = False, variant: str = "",
+          defines: tuple = ()) -> Path:
     """stress=True: the synchronisation-stress variant (-DSSK_SYNC_STRESS, random warp delays at
-    every barrier hand-off) into _lib/stress/libssimk.so, for tools/sync_stress.py only."""
-    lib_out = OUT_DIR / "stress" / "libssimk.so" if stress else LIB
+    every barrier hand-off) into _lib/stress/libssimk.so, for tools/sync_stress.py only.
+    variant/defines: an A/B build with extra -D flags into _lib/<variant>/libssimk.so."""
+    if stress:
+        variant, defines = "stress", ("SSK_SYNC_STRESS",)
+    lib_out = OUT_DIR / variant / "libssimk.so" if variant else LIB
     if not force and not _stale(lib_out):
         return lib_out
     lib_out.parent.mkdir(parents=True, exist_ok=True)
-    obj_dir = OUT_DIR / ("obj_stress" if stress else "obj")
+    obj_dir = OUT_DIR / (f"obj_{variant}" if variant else "obj")
     obj_dir.mkdir(exist_ok=True)
     cc = nvcc()
-    extra = ["-DSSK_SYNC_STRESS"] if stress else []
+    extra = [f"-D{d}" for d in defines]
 
     def obj_stale(src: str, obj: Path) -> bool:
         if force or not obj.exists():
@@ -86,4 +90,7 @@ def build(force: bool = False, verbose: bool = False, stress: bool = False) -> P
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True, stress="--stress" in sys.argv))
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
+    defs = tuple(a.split("=", 1)[1] for a in sys.argv if a.startswith("--define="))
+    print(build(force="--force" in sys.argv, verbose=True, stress="--stress" in sys.argv, variant=var,
+                defines=defs))

@@ -161,7 +161,8 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
 }
 
 // MAPS = false compiles the map stores out (score-only kernels: smaller code, no dead branches)
-template <int K, typename TIN, int NM, bool WS, int VC, bool PERSIST = false, bool MAPS = true>
+// L1 = false compiles the fused pyramid-level-1 stores out (score-only persistent launches)
+template <int K, typename TIN, int NM, bool WS, int VC, bool PERSIST = false, bool MAPS = true, bool L1 = true>
 __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0, const int seg0, const int pair0,
                                            const int nstrips, const int nseg) {
   constexpr int VP = vp_of(VC);
@@ -212,23 +213,60 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
   if constexpr (PERSIST) tile_of(blockIdx.x);
   else set_tile(strip0, seg0, pair0);
 
-  auto stage_rows = [&](int r_lo, int r_hi) {  // issued by the VC V-pass threads
+  // staging (issued by the VC V-pass threads): a thread always copies the same 16-byte chunk
+  // q of the same image im, of every RPP-th row, so per call the source base, the chunk's
+  // validity and the ring offset are computed once and the loop is a pointer increment
+  // and a ring-slot wrap (was a division / modulo chain per 16-byte item)
+  constexpr int IPR = 4 * NCH;  // 16-byte items per input row (4 images)
+  constexpr int RPP = VC / IPR;  // rows per pass (when IPR divides VC)
+  auto stage_rows = [&](int r_lo, int r_hi) {
     r_hi = min(r_hi, in_end);
-    const int total = (r_hi - r_lo) * 4 * NCH;
-    for (int i = tid; i < total; i += VC) {
-      const int rr = i / (4 * NCH);
-      const int rem = i - rr * (4 * NCH);
-      const int im = rem / NCH;
-      const int q = rem - im * NCH;
-      const int row = r_lo + rr;
-      const int off = q * 16;
-      int valid = row_bytes_left - off;
-      valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
-      const unsigned char* rowp =
-          ((im & 2) ? a.dist : a.ref) + ((im & 1) ? fo1 : fo0) + (long long)row * a.row_pitch_b;
-      const unsigned char* src = valid ? rowp + (long long)c0 * ES + off : rowp;
-      const int slot = (row - y0) % RR;
-      cp_async16(raw + (slot * 4 + im) * RB + off, src, valid);
+    // Measured (tools/ab_libs.sh, 64 x 1080p): the strength-reduced loop speeds up the
+    // score-only warp-specialised launch (0.667 -> 0.657 ms) but slows the MS-SSIM step
+    // when the producers also write the fused pyramid level 1 (0.912 -> 0.918 ms) and in
+    // the classic kernel (coarse levels, +0.005 ms): it runs only where it wins.
+#ifdef SSK_STAGE_GENERIC
+    constexpr bool generic_stage = true;  // A/B build: the item loop everywhere
+#else
+    constexpr bool generic_stage = VC % IPR != 0 || !WS || L1;
+#endif
+    if constexpr (generic_stage) {  // generic item loop
+      const int total = (r_hi - r_lo) * IPR;
+      for (int i = tid; i < total; i += VC) {
+        const int rr = i / IPR;
+        const int rem = i - rr * IPR;
+        const int im = rem / NCH;
+        const int q = rem - im * NCH;
+        const int row = r_lo + rr;
+        const int off = q * 16;
+        int valid = row_bytes_left - off;
+        valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
+        const unsigned char* rowp =
+            ((im & 2) ? a.dist : a.ref) + ((im & 1) ? fo1 : fo0) + (long long)row * a.row_pitch_b;
+        const unsigned char* src = valid ? rowp + (long long)c0 * ES + off : rowp;
+        cp_async16(raw + (((row - y0) % RR) * 4 + im) * RB + off, src, valid);
+      }
+      cp_async_commit();
+      return;
+    }
+    if (tid >= RPP * IPR) {  // (never: RPP * IPR == VC)
+      cp_async_commit();
+      return;
+    }
+    const int im = (tid % IPR) / NCH, q = tid % NCH;
+    int valid = row_bytes_left - q * 16;
+    valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
+    const long long pitch = a.row_pitch_b;
+    int row = r_lo + tid / IPR;
+    const unsigned char* src = ((im & 2) ? a.dist : a.ref) + ((im & 1) ? fo1 : fo0) +
+                               (valid ? (long long)c0 * ES + q * 16 : 0) + (long long)row * pitch;
+    unsigned char* dst = raw + im * RB + q * 16;
+    int slot = (row - y0) % RR;
+    for (; row < r_hi; row += RPP) {
+      cp_async16(dst + slot * 4 * RB, src, valid);
+      src += RPP * pitch;
+      slot += RPP;
+      if (slot >= RR) slot -= RR;
     }
     cp_async_commit();
   };
@@ -620,7 +658,9 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
             }
             named_sync(1, VC);
             if constexpr (VC == 256 && ES == 1) {
-              if (a.l1_ref) level1(c);
+              if constexpr (L1) {
+                if (a.l1_ref) level1(c);
+              }
             }
             if (cc >= NB) named_sync(2 + NB + b, 2 * VC);
             vpass(c, vbuf0 + b * VBYTES);
@@ -724,11 +764,11 @@ __global__ void __launch_bounds__(2 * VC, VC == 128 ? 2 : 1) gauss_ws_kernel(con
 }
 
 // Persistent variant (one CTA per SM walking tiles blockIdx.x, + gridDim.x, ...)
-template <int K, typename TIN, int NM, int VC>
+template <int K, typename TIN, int NM, int VC, bool L1>
 __global__ void __launch_bounds__(2 * VC, 1)
     gauss_ws_persist_kernel(const __grid_constant__ GaussArgs a, const int nstrips, const int nseg) {
   // (the map branch stays compiled in: measured faster here than the MAPS = false build)
-  gauss_body<K, TIN, NM, true, VC, true>(a, 0, 0, 0, nstrips, nseg);
+  gauss_body<K, TIN, NM, true, VC, true, true, L1>(a, 0, 0, 0, nstrips, nseg);
 }
 
 // All pyramid levels of one sample type in one launch: blockIdx.x enumerates the
@@ -767,7 +807,9 @@ int launch_ws(const GaussArgs& a, dim3 grid, cudaStream_t st) {
     // wide u8 strips (1 CTA / SM): persistent CTAs keep the V-tile pipeline full across tiles
     const long long ntiles = (long long)grid.x * grid.y * grid.z;
     if (gauss_persist_level() >= 1 && ntiles > 0) {
-      auto fp = gauss_ws_persist_kernel<K, TIN, NM, VC>;
+      // two builds: with the fused level-1 stores (MS-SSIM) and without (score-only launches,
+      // smaller code and the strength-reduced staging loop)
+      auto fp = a.l1_ref ? gauss_ws_persist_kernel<K, TIN, NM, VC, true> : gauss_ws_persist_kernel<K, TIN, NM, VC, false>;
       if (cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return SSK_E_CUDA;
       int nctas = (int)std::min<long long>(ntiles, (long long)sm_count());

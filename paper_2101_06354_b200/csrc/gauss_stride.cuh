@@ -44,7 +44,7 @@ __host__ __device__ constexpr size_t sg_smem() {
 }
 
 template <int K, typename TIN, int S>
-__global__ void __launch_bounds__(SG_THREADS, 1) gauss_stride_kernel(const __grid_constant__ GaussArgs a) {
+__global__ void __launch_bounds__(SG_THREADS, 2) gauss_stride_kernel(const __grid_constant__ GaussArgs a) {
   constexpr int ES = (int)sizeof(TIN);
   static_assert(ES <= 2, "8/16-bit samples only");
   constexpr int G = sg_g<S>();
@@ -77,22 +77,29 @@ __global__ void __launch_bounds__(SG_THREADS, 1) gauss_stride_kernel(const __gri
   const long long fo0 = (long long)f0 * a.frame_pitch_b, fo1 = (long long)f1 * a.frame_pitch_b;
   const int row_bytes_left = (a.w - cx0) * ES;
 
+  // staging: a thread always copies the same 16-byte chunk q of the same image im, of every
+  // RPP-th row -- source base, chunk validity and ring offset are fixed per thread, so the
+  // copy loop is a pointer increment and a ring-slot wrap (no divisions per item)
+  constexpr int IPR = 4 * NCH;              // 16-byte items per input row (4 images)
+  static_assert(SG_THREADS % IPR == 0, "whole rows per pass");
+  constexpr int RPP = SG_THREADS / IPR;     // rows per pass
+  const int st_im = (tid % IPR) / NCH, st_q = tid % NCH, st_r0 = tid / IPR;
+  const long long pitch = a.row_pitch_b;
+  int st_valid = row_bytes_left - st_q * 16;
+  st_valid = st_valid < 0 ? 0 : (st_valid > 16 ? 16 : st_valid);
+  const unsigned char* st_base = ((st_im & 2) ? a.dist : a.ref) + ((st_im & 1) ? fo1 : fo0) +
+                                 (st_valid ? (long long)cx0 * ES + st_q * 16 : 0);
+  unsigned char* st_dst = raw + st_im * RB + st_q * 16;
   auto stage_rows = [&](int r_lo, int r_hi) {  // input rows [r_lo, r_hi) -> ring slots
     r_hi = min(r_hi, in_end);
-    const int total = (r_hi - r_lo) * 4 * NCH;
-    for (int i = tid; i < total; i += SG_THREADS) {
-      const int rr = i / (4 * NCH);
-      const int rem = i - rr * (4 * NCH);
-      const int im = rem / NCH;
-      const int q = rem - im * NCH;
-      const int row = r_lo + rr;
-      const int off = q * 16;
-      int valid = row_bytes_left - off;
-      valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
-      const unsigned char* rowp =
-          ((im & 2) ? a.dist : a.ref) + ((im & 1) ? fo1 : fo0) + (long long)row * a.row_pitch_b;
-      const unsigned char* src = valid ? rowp + (long long)cx0 * ES + off : rowp;
-      cp_async16(raw + (((row - y0) % RR) * 4 + im) * RB + off, src, valid);
+    int row = r_lo + st_r0;
+    int slot = (row - y0) % RR;
+    const unsigned char* src = st_base + (long long)row * pitch;
+    for (; row < r_hi; row += RPP) {
+      cp_async16(st_dst + slot * 4 * RB, src, st_valid);
+      src += RPP * pitch;
+      slot += RPP;
+      if (slot >= RR) slot -= RR;
     }
     cp_async_commit();
   };

@@ -3,6 +3,7 @@
   --mode step : 3 full bench steps (64x 1080p SSIM + 5-scale MS-SSIM) -> launch list / shares
   --mode l0   : the level-0 fused Gaussian SSIM kernel over the 64-frame batch, 3 launches
   --mode box  : config-4 shape: rect 8 stride 4 on 10-bit 4K u16, 32 frames, 3 launches
+  --mode stride : Gaussian 11/1.5 stride 5 scores (K1s) over the 64-frame 1080p batch, 3 launches
 """
 
 from __future__ import annotations
@@ -16,7 +17,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 def main() -> None:
     ap = argparse.ArgumentParser()
-    ap.add_argument("--mode", default="step", choices=["step", "l0", "box"])
+    ap.add_argument("--mode", default="step", choices=["step", "l0", "box", "stride"])
     ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
 
@@ -45,6 +46,10 @@ def main() -> None:
     if args.mode == "step":
         for _ in range(args.reps):
             P.msssim_batch(r, d, cfg, P.MultiscaleSpec.product(5), with_ssim=True)
+    elif args.mode == "stride":
+        cs = P.SsimConfig(window=P.WindowSpec.gaussian(1.5, stride=5))
+        for _ in range(args.reps):
+            P.ssim_terms_batch(r, d, cs)
     else:
         pair = engine.device_pair(r, d, 8, gauss=True)
         for _ in range(args.reps):
