@@ -1032,3 +1032,30 @@ def test_stats_and_term_maps_api_bit_exact(cuda, oracle, rng):
     assert np.array_equal(maps.q_map.values, wq)
     one = moments.stats_from_sums(np.float64(10.0), s2, q1, q2, p12, 121.0)[0]
     assert one.shape == shape and np.all(one == 10.0 / 121.0)
+
+
+def test_c_host_program_end_to_end(cuda, oracle, tmp_path):
+    """A C program using only the C ABI + the CUDA runtime (tests/c_abi/ssim_cli.c: library-built
+    Gaussian taps from sigma, ssk_ssim + ssk_msssim) scores a pair like the oracle does."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from test_native_abi import build_c_cli
+    from paper_2101_06354_b200 import synth
+
+    exe = build_c_cli(tmp_path)
+    rng = np.random.default_rng(99)
+    h, w = 300, 517
+    a = synth.inv_f_noise(rng, h, w, 255.0).astype(np.uint8)
+    b = np.clip(a.astype(int) + rng.integers(-15, 16, a.shape), 0, 255).astype(np.uint8)
+    (tmp_path / "a.u8").write_bytes(a.tobytes())
+    (tmp_path / "b.u8").write_bytes(b.tobytes())
+    r = subprocess.run([str(exe), str(h), str(w), str(tmp_path / "a.u8"), str(tmp_path / "b.u8"), "1.5", "3"],
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    f = r.stdout.split()
+    win = dict(shape="gauss", k=11, sigma=1.5)
+    assert max(abs(float(x) - y) for x, y in zip(f[1:4], oracle.ssim_terms(a, b, **win))) < SCORE_TOL
+    assert abs(float(f[5]) - oracle.msssim(a, b, 3, **win)) < SCORE_TOL

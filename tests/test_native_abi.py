@@ -149,3 +149,23 @@ def test_wide_gaussian_windows_plan_with_sigma():
     assert _gauss_call(_gauss_window(k=257, sigma=40.0), 300, 300) == 0
     assert _gauss_call(_gauss_window(k=255, sigma=40.0), 300, 300) > 0
     assert _gauss_call(_gauss_window(k=37, sigma=6.0), 30, 300) == 0   # window larger than image
+
+
+def build_c_cli(out_dir):
+    """Compile tests/c_abi/ssim_cli.c -- a host program using only the C ABI -- with gcc."""
+    exe = Path(out_dir) / "ssim_cli"
+    cmd = ["gcc", "-std=c99", "-O2", "-Wall", "-Werror", "-I", str(REPO / "include"), "-I", "/usr/local/cuda/include",
+           str(REPO / "tests" / "c_abi" / "ssim_cli.c"), "-o", str(exe), "-L", str(nat.LIB_PATH.parent), "-lssimk",
+           f"-Wl,-rpath,{nat.LIB_PATH.parent}", "-L", "/usr/local/cuda/lib64", "-lcudart",
+           "-Wl,-rpath,/usr/local/cuda/lib64"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+@pytest.mark.skipif(shutil.which("gcc") is None or not Path("/usr/local/cuda/include/cuda_runtime.h").exists(),
+                    reason="needs gcc and the CUDA headers")
+def test_c_host_program_compiles_against_the_abi(tmp_path):
+    """include/ssimk.h is plain C99 and libssimk.so links into a C program (no C++, no torch)."""
+    exe = build_c_cli(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 1 and "usage" in r.stderr
