@@ -251,7 +251,8 @@ enum {
   SSK_POOL_DW = 4,   /* sum((1-v)^p v) / sum((1-v)^p), mean if all v == 1    */
   SSK_POOL_MINK = 5, /* mean (1-v)^p                                          */
   SSK_POOL_LW = 6,   /* mean w(mu) v, w = [mu >= a] (b == 0) or clip((mu-a)/b) */
-  SSK_POOL_PP = 7    /* mean of v/rs below the ps-th percentile, v above     */
+  SSK_POOL_PP = 7,   /* mean of v/rs below the ps-th percentile, v above     */
+  SSK_POOL_PCTL = 8  /* np.percentile(v, ps) itself (pp's cutoff; exact)     */
 };
 
 typedef struct ssk_maps {
@@ -270,6 +271,28 @@ typedef struct ssk_pooler {
   double a, b;               /* lw lower luminance limit, ramp length                    */
   double ps, rs;             /* pp percentile, down-weighting divisor                    */
 } ssk_pooler;
+
+/* numpy-order sums for the per-map pooling API: for each of the n maps (row-major
+ * flattened, as pool_spatial's v.reshape(-1)), the sum of an elementwise fp64 expression in
+ * np.add.reduce's pairwise order (PW_BLOCKSIZE 128, starting from 0.0) -- bit-identical to
+ * the reference's numpy reductions on the same values (src/pooling.py:157-243):
+ *   SSK_PW_V            v
+ *   SSK_PW_SQDEV        (v - c)^2                 np.std's second pass (c = the mean)
+ *   SSK_PW_ABSDEV_P     |v - c| ** p              md
+ *   SSK_PW_ONEMINUS_P   (1 - v) ** p              mink, dw's total
+ *   SSK_PW_DW_NUM       ((1 - v) ** p) * v        dw
+ *   SSK_PW_PP           v <= c ? v / p : v        pp (c = the cutoff, p = rs)
+ *   SSK_PW_LW           w(aux) * v                lw: w = aux >= a (b == 0), else
+ *                                                 clip((aux - a) / b, 0, 1)
+ * d_c: per-map centre [n] (NULL when unused).  `** p` follows numpy's fast scalar powers
+ * (2, 1, 0.5, -1, 0); integer p in [3, 64] is computed in double-double and rounded once
+ * (libm pow's correctly rounded result in practice); other p use CUDA pow (<= 2 ulp).
+ * Workspace: ssk_pairwise_workspace_bytes(m). */
+enum { SSK_PW_V = 0, SSK_PW_SQDEV = 1, SSK_PW_ABSDEV_P = 2, SSK_PW_ONEMINUS_P = 3, SSK_PW_DW_NUM = 4,
+       SSK_PW_PP = 5, SSK_PW_LW = 6 };
+size_t ssk_pairwise_workspace_bytes(const ssk_maps* m);
+int ssk_pairwise_sum(const ssk_maps* m, int expr, double p, double a, double b, const double* d_c, double* d_out,
+                     void* d_workspace, size_t workspace_bytes, void* stream);
 
 size_t ssk_pool_workspace_bytes(const ssk_maps* m, const ssk_pooler* pool);
 /* CoV / MD(p = 2, o) pooling without a map, from the [n][4] per-frame sums of an

@@ -32,6 +32,7 @@ LIB_PATH = Path(os.environ.get("SSK_LIBRARY") or Path(__file__).resolve().parent
 U8, U16, U32, F32, F64 = 1, 2, 3, 4, 5
 RECT, GAUSS = 1, 2
 WANT_Q, WANT_L, WANT_CS, MAP_TERMS, MAP_STATS, WANT_Q2, MAP_F64 = 1, 2, 4, 8, 16, 32, 64
+PW_V, PW_SQDEV, PW_ABSDEV_P, PW_ONEMINUS_P, PW_DW_NUM, PW_PP, PW_LW = range(7)
 E_ARG, E_WINDOW, E_SHAPE, E_WORKSPACE, E_ALIGN, E_CUDA, E_LEVELS, E_TOO_SMALL = range(-1, -9, -1)
 
 ABI_VERSION = 9
@@ -40,6 +41,8 @@ GAUSS_MAX_K = 255  # SSK_GAUSS_MAX_K
 EXPORTED_SYMBOLS = (
     "ssk_abi_version",
     "ssk_stats_from_sums",
+    "ssk_pairwise_workspace_bytes",
+    "ssk_pairwise_sum",
     "ssk_term_maps",
     "ssk_divide",
     "ssk_strerror",
@@ -74,6 +77,7 @@ CONV_RGB, CONV_YCBCR, CONV_LUMA, CONV_HUE, CONV_LAB_EMBED = 1, 2, 3, 4, 5
 
 # spatial pooler kinds (SSK_POOL_*), in SPATIAL_KINDS order of src/pooling.py:29
 POOL_KINDS = {"am": 0, "cov": 1, "md": 2, "fns": 3, "dw": 4, "mink": 5, "lw": 6, "pp": 7}
+POOL_PCTL = 8  # np.percentile(v, ps) itself (SSK_POOL_PCTL)
 
 
 class Planes(ctypes.Structure):
@@ -182,6 +186,11 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         lib.ssk_ssim_workspace_bytes.argtypes = [pP, pW]
         lib.ssk_msssim_workspace_bytes.restype = sz
         lib.ssk_msssim_workspace_bytes.argtypes = [pP, pW, i32]
+        lib.ssk_pairwise_workspace_bytes.restype = sz
+        lib.ssk_pairwise_workspace_bytes.argtypes = [ctypes.POINTER(Maps)]
+        lib.ssk_pairwise_sum.restype = i32
+        lib.ssk_pairwise_sum.argtypes = [ctypes.POINTER(Maps), i32, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_double, vp, vp, vp, sz, vp]
         lib.ssk_stats_from_sums.restype = i32
         lib.ssk_stats_from_sums.argtypes = [vp, vp, vp, vp, vp, i64, ctypes.c_double, vp, vp]
         lib.ssk_term_maps.restype = i32

@@ -1,9 +1,11 @@
 """Channel-wise color SSIM (ssimkit src/color.py, cw/fixed models) on the B200.
 
 Each channel is scored at its own resolution (4:2:0 chroma is not
-upsampled, src/color.py:122-125, :144-153) by the fused SSIM kernel; only the
-three per-channel means return to the host, where they are combined in
-float64 with the reference's formulas.  The BT.709 conversions needed to
+upsampled, src/color.py:122-125, :144-153) as the reference defines it,
+mssim(ssim_map(..)): the map stays on the device and its mean is taken in
+numpy's pairwise order; only the three per-channel means return to the host,
+where they are combined in float64 with the reference's formulas.  (The
+throughput path, ``batch.color_batch``, uses the fused score kernels.)  The BT.709 conversions needed to
 accept RGB input run on the device (``colorimetric.py``, src/color.py:64-108),
 as do the quaternion / CIELAB / hue models.
 """
@@ -15,7 +17,7 @@ import numpy as np
 from .errors import DegenerateWeights, ValidationError, WrongSpace
 from .options import SsimConfig
 from .planes import CHROMA_444, SPACE_RGB, SPACE_YCBCR, ColorFrame, validate_color_pair
-from .scoring import ssim_score
+from .scoring import map_mean_score
 
 from .colorimetric import luma_of, rgb_to_ycbcr_bt709, ycbcr_bt709_to_rgb  # noqa: F401  (device conversions)
 
@@ -45,7 +47,9 @@ def channel_scores(ref: ColorFrame, dist: ColorFrame, config: SsimConfig) -> tup
     elif ref.space != SPACE_YCBCR:
         raise WrongSpace(f"channel-wise scoring needs RGB or YCbCr frames, got {ref.space}")
     config = config.for_bit_depth(ref.bit_depth)
-    return tuple(ssim_score(a, b, config) for a, b in zip(ref.channels, dist.channels))
+    # the reference's own definition, mssim(ssim_map(..)) per plane: the map on the device
+    # (fp64 for Gaussian windows, exact for rect) and its numpy-order mean (ssk_pairwise_sum)
+    return tuple(map_mean_score(a, b, config) for a, b in zip(ref.channels, dist.channels))
 
 
 def channelwise_cssim(ref: ColorFrame, dist: ColorFrame, alpha: float, beta: float,

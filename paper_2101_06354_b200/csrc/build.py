@@ -17,7 +17,7 @@ REPO = PKG.parent
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libssimk.so"
 SOURCES = ["gauss_ssim.cu", "gauss_generic.cu", "gauss_stride.cu", "gauss_stride_s2.cu", "gauss_stride_s3.cu", "gauss_stride_s4.cu", "gauss_stride_s5.cu", "gauss_stride_s6.cu", "gauss_stride_s7.cu", "gauss_stride_s8.cu", "gauss_u8.cu", "gauss_u16.cu", "gauss_u32.cu", "gauss_f32.cu", "box_ssim.cu",
-           "box_block.cu", "volume.cu", "aux_kernels.cu", "pool_adapt.cu", "color_models.cu", "capi.cu"]
+           "box_block.cu", "volume.cu", "aux_kernels.cu", "pool_adapt.cu", "pool_exact.cu", "color_models.cu", "capi.cu"]
 HEADERS = ["common.cuh", "kernels.h", "gauss_ssim.cuh", "gauss_stride.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

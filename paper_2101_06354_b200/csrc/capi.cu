@@ -832,6 +832,23 @@ int ssk_divide(const double* d_x, int64_t count, double divisor, double* d_out, 
   return launch_divide(d_x, count, divisor, d_out, static_cast<cudaStream_t>(stream));
 }
 
+size_t ssk_pairwise_workspace_bytes(const ssk_maps* m) {
+  if (!m || m->n < 1 || m->h < 1 || m->w < 1) return 0;
+  return pairwise_workspace_bytes(m);
+}
+
+int ssk_pairwise_sum(const ssk_maps* m, int expr, double p, double a, double b, const double* d_c, double* d_out,
+                     void* d_workspace, size_t workspace_bytes, void* stream) {
+  if (!m || !m->values || !d_out || m->n < 1 || m->h < 1 || m->w < 1 || m->n > 65535) return SSK_E_ARG;
+  if (m->dtype != SSK_F32 && m->dtype != SSK_F64) return SSK_E_ARG;
+  if (m->row_pitch < m->w || m->frame_pitch < m->row_pitch * (int64_t)m->h) return SSK_E_ARG;
+  if (expr < SSK_PW_V || expr > SSK_PW_LW) return SSK_E_ARG;
+  if ((expr == SSK_PW_SQDEV || expr == SSK_PW_ABSDEV_P || expr == SSK_PW_PP) && !d_c) return SSK_E_ARG;
+  if (expr == SSK_PW_LW && (!m->aux || m->aux_row_pitch < m->w)) return SSK_E_ARG;
+  if (!d_workspace || workspace_bytes < pairwise_workspace_bytes(m)) return SSK_E_WORKSPACE;
+  return launch_pairwise_maps(m, expr, p, a, b, d_c, d_out, d_workspace, static_cast<cudaStream_t>(stream));
+}
+
 uint64_t ssk_launch_count(void) { return g_launches.load(); }
 
 int ssk_host_register(void* ptr, size_t bytes, int read_only) {

@@ -59,6 +59,11 @@ int launch_gauss_u16(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 int launch_gauss_u32(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 int launch_gauss_f32(const GaussArgs& a, dim3 grid, int k, cudaStream_t st);
 
+// ---------------- numpy-order map sums for the per-map pooling API (pool_exact.cu) ----------------
+size_t pairwise_workspace_bytes(const ssk_maps* m);
+int launch_pairwise_maps(const ssk_maps* m, int expr, double p, double a, double b, const double* d_c,
+                         double* d_out, void* d_ws, cudaStream_t st);
+
 // ---------------- elementwise map arithmetic of the public API (aux_kernels.cu) ----------------
 int launch_stats_from_sums(const double* s1, const double* s2, const double* q1, const double* q2,
                            const double* p12, long long count, double area, double* out, cudaStream_t st);

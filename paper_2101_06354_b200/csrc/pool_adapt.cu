@@ -218,6 +218,9 @@ __device__ void finish(const PoolArgs& a, int frame, double sum, double mn, doub
     case SSK_POOL_PP:
       r = (a.ps <= 0.0 || a.rs == 1.0) ? mean : __ddiv_rn(s2, a.cnt);
       break;
+    case SSK_POOL_PCTL:
+      r = np_lerp(rank_value<T>(a, frame, 0), rank_value<T>(a, frame, 1), a.gamma[0]);
+      break;
     default:
       break;
   }
@@ -722,7 +725,7 @@ int plan_pool(const ssk_maps* m, const ssk_pooler* pl, PoolPlan& P) {
   if (m->n < 1 || m->n > 65535 || m->h < 1 || m->w < 1) return SSK_E_ARG;
   if (m->row_pitch < m->w || m->frame_pitch < m->row_pitch * (int64_t)m->h) return SSK_E_ARG;
   const int kind = pl->kind;
-  if (kind < SSK_POOL_AM || kind > SSK_POOL_PP) return SSK_E_ARG;
+  if (kind < SSK_POOL_AM || kind > SSK_POOL_PCTL) return SSK_E_ARG;
   if ((kind == SSK_POOL_MD || kind == SSK_POOL_DW || kind == SSK_POOL_MINK) && !(pl->p > 0)) return SSK_E_ARG;
   if (kind == SSK_POOL_MD && !(pl->o > 0)) return SSK_E_ARG;
   if (kind == SSK_POOL_LW) {
@@ -730,6 +733,7 @@ int plan_pool(const ssk_maps* m, const ssk_pooler* pl, PoolPlan& P) {
     if (m->aux_row_pitch < m->w || m->aux_frame_pitch < m->aux_row_pitch * (int64_t)m->h) return SSK_E_ARG;
   }
   if (kind == SSK_POOL_PP && !(pl->ps >= 0 && pl->ps <= 100 && pl->rs >= 1)) return SSK_E_ARG;
+  if (kind == SSK_POOL_PCTL && !(pl->ps >= 0 && pl->ps <= 100)) return SSK_E_ARG;
   PoolArgs& a = P.a;
   a.vals = static_cast<const unsigned char*>(m->values);
   a.aux = static_cast<const unsigned char*>(m->aux);
@@ -765,7 +769,7 @@ int plan_pool(const ssk_maps* m, const ssk_pooler* pl, PoolPlan& P) {
     qs[1] = 50.0 / 100.0;
     qs[2] = 75.0 / 100.0;
     nq = 3;
-  } else if (kind == SSK_POOL_PP && !(pl->ps <= 0.0 || pl->rs == 1.0)) {
+  } else if ((kind == SSK_POOL_PP && !(pl->ps <= 0.0 || pl->rs == 1.0)) || kind == SSK_POOL_PCTL) {
     qs[0] = pl->ps / 100.0;
     nq = 1;
   }

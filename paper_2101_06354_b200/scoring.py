@@ -89,6 +89,17 @@ def mssim(maps: Union[SsimTermMaps, QualityMap, np.ndarray]) -> float:
     return pool_spatial(v, "am")
 
 
+def map_mean_score(ref: PlaneLike, dist: PlaneLike, config: SsimConfig = SsimConfig()) -> float:
+    """mssim(ssim_map(ref, dist, config)) without the map leaving the device: the q map
+    (fp64 for Gaussian windows) and its numpy-order mean (``ssk_pairwise_sum``), i.e. the
+    reference's definition of a plane's score, bit for bit where the maps are."""
+    from .pooling import SpatialPooler, _pool_exact
+
+    pair, _ = _prepare(ref, dist, config)
+    _, maps = engine.ssim(pair, config.window, config.c1, config.c2, nat.WANT_Q | nat.MAP_TERMS | nat.MAP_F64)
+    return _pool_exact(maps[0, 2], SpatialPooler("am"))
+
+
 def ssim_terms(ref: PlaneLike, dist: PlaneLike, config: SsimConfig = SsimConfig()) -> tuple[float, float, float]:
     """(mean q, mean l, mean cs) of a pair from one fused pass; no map leaves the GPU."""
     pair, (h, w) = _prepare(ref, dist, config)

@@ -123,8 +123,11 @@ def test_color_against_golden(cuda, golden):
     assert abs(P.channelwise_cssim(ref, dist, -0.3, -0.3, cfg) - float(golden["color/cw"])) < SCORE_TOL
     per = np.array(P.channel_scores(ref, dist, cfg))
     assert np.max(np.abs(per - golden["color/per_plane"])) < SCORE_TOL
-    # (1, 0, 0) weights reduce to the luma score exactly (tests/test_color.py:109-114)
-    assert P.fixed_weight_cssim(ref, dist, (1.0, 0.0, 0.0), cfg) == P.ssim_score(ref.channels[0], dist.channels[0], cfg)
+    # (1, 0, 0) weights reduce to the luma score exactly (tests/test_color.py:109-114): a plane's
+    # score is mssim(ssim_map(..)) as in the reference; the fused score path agrees to fp32
+    luma = P.mssim(P.ssim_map(ref.channels[0], dist.channels[0], cfg))
+    assert P.fixed_weight_cssim(ref, dist, (1.0, 0.0, 0.0), cfg) == luma
+    assert abs(P.ssim_score(ref.channels[0], dist.channels[0], cfg) - luma) < SCORE_TOL
 
 
 def test_config1_score(cuda, golden):

@@ -71,8 +71,10 @@ def test_pool_maps_batch_equals_single(cuda, oracle):
         for i in range(6):
             single, _ = P.pool_maps(tm[i], sel, tl[i])
             assert float(batched[i]) == float(single[0])
+            # the per-map API reduces in numpy's order (bit-exact to numpy), the batch in a
+            # fixed tree order: equal to rounding
             want = P.pool_spatial(maps[i], sel, ref_luma=luma[i])
-            assert float(batched[i]) == want
+            assert abs(float(batched[i]) - want) <= 1e-14 * max(1.0, abs(want))
         assert np.allclose(means.cpu().numpy(), maps.reshape(6, -1).mean(axis=1), rtol=1e-14)
     # strided views (a plane of an [n, 3, h, w] map stack) pool in place
     stack = torch.from_numpy(rng.uniform(0, 1, (4, 3, 20, 30))).to(cuda)
@@ -193,3 +195,28 @@ def test_fused_moment_pooling_matches_map_pooling(cuda):
             q = P.ssim_map(a, b, P.SsimConfig(window=win)).q_map
             assert fused.score == pytest.approx(P.pool_spatial(q, sel), rel=1e-10, abs=1e-14), (win, sel)
             assert fused.am == pytest.approx(float(q.values.mean()), abs=1e-14)
+
+
+POOL_EXACT_CASES = [
+    ("am", {}), ("cov", {}), ("md", {"p": 2.0, "o": 3.0}), ("md", {"p": 1.0, "o": 1.0}), ("md", {"p": 3.0, "o": 1.0}),
+    ("dw", {"p": 2.0}), ("dw", {"p": 1.0}), ("dw", {"p": 4.0}), ("mink", {"p": 4.0}), ("mink", {"p": 2.0}),
+    ("pp", {"ps": 10.0, "rs": 3.0}), ("pp", {"ps": 6.0, "rs": 4000.0}), ("lw", {"a": 40.0, "b": 0.0}),
+    ("lw", {"a": 20.0, "b": 50.0}), ("fns", {}),
+]
+
+
+@pytest.mark.parametrize("shape", [(6, 6), (5, 8), (37, 53), (502, 502), (1070, 1910)])
+@pytest.mark.parametrize("kind,kw", POOL_EXACT_CASES)
+def test_pool_spatial_bit_exact_vs_numpy(cuda, oracle, shape, kind, kw):
+    """The per-map pool_spatial (src/pooling.py:202-243) reduces in numpy's pairwise order on
+    the device (ssk_pairwise_sum) and finishes with the reference's scalar expressions: equal
+    to numpy's value bit for bit (integer exponents through the correctly rounded power)."""
+    import paper_2101_06354_b200 as P
+
+    rng = np.random.default_rng(shape[0] * 7919 + shape[1] * 31 + len(kind))
+    v = 1.0 - 0.3 * rng.uniform(0, 1, shape) ** 3
+    mu = rng.uniform(0.0, 255.0, shape)
+    pool = P.SpatialPooler(kind, **kw)
+    got = P.pool_spatial(v, pool, ref_luma=mu if kind == "lw" else None)
+    want = oracle.pool_spatial(v, kind, ref_luma=mu if kind == "lw" else None, **kw)
+    assert got == want, (got, want)
