@@ -247,28 +247,24 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
         cp_async16(raw + (((row - y0) % RR) * 4 + im) * RB + off, src, valid);
       }
       cp_async_commit();
-      return;
-    }
-    if (tid >= RPP * IPR) {  // (never: RPP * IPR == VC)
+    } else {  // strength-reduced loop
+      const int im = (tid % IPR) / NCH, q = tid % NCH;
+      int valid = row_bytes_left - q * 16;
+      valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
+      const long long pitch = a.row_pitch_b;
+      int row = r_lo + tid / IPR;
+      const unsigned char* src = ((im & 2) ? a.dist : a.ref) + ((im & 1) ? fo1 : fo0) +
+                                 (valid ? (long long)c0 * ES + q * 16 : 0) + (long long)row * pitch;
+      unsigned char* dst = raw + im * RB + q * 16;
+      int slot = (row - y0) % RR;
+      for (; row < r_hi; row += RPP) {
+        cp_async16(dst + slot * 4 * RB, src, valid);
+        src += RPP * pitch;
+        slot += RPP;
+        if (slot >= RR) slot -= RR;
+      }
       cp_async_commit();
-      return;
     }
-    const int im = (tid % IPR) / NCH, q = tid % NCH;
-    int valid = row_bytes_left - q * 16;
-    valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
-    const long long pitch = a.row_pitch_b;
-    int row = r_lo + tid / IPR;
-    const unsigned char* src = ((im & 2) ? a.dist : a.ref) + ((im & 1) ? fo1 : fo0) +
-                               (valid ? (long long)c0 * ES + q * 16 : 0) + (long long)row * pitch;
-    unsigned char* dst = raw + im * RB + q * 16;
-    int slot = (row - y0) % RR;
-    for (; row < r_hi; row += RPP) {
-      cp_async16(dst + slot * 4 * RB, src, valid);
-      src += RPP * pitch;
-      slot += RPP;
-      if (slot >= RR) slot -= RR;
-    }
-    cp_async_commit();
   };
 
   if (tid < VC) stage_rows(y0, y0 + G + K - 1);  // (persistent CTAs: their first tile)
