@@ -73,3 +73,27 @@ def test_msssim_fuzz_wide_and_classic(cuda, oracle):
         got = P.scale_scores(a, b, rect, levels)
         want = oracle.scale_scores(a, b, levels, shape="rect", k=k)
         assert np.max(np.abs(np.array(got) - np.array(want))) < 1e-12
+
+
+def test_strided_gauss_fuzz(cuda, oracle):
+    """Anchor-only strided Gaussian scores (K1s for s = 2..8, K1 masking above) over random
+    geometries, window sizes, strides and 8/10-bit samples, batches of 1-3 frames."""
+    import torch
+
+    rng = np.random.default_rng(313)
+    for _ in range(40):
+        k = int(rng.choice([3, 5, 7, 9, 11, 13, 15, 21, 31]))
+        sigma = float(rng.uniform(0.4, max(0.5, k / 6.0)))
+        s = int(rng.integers(2, 11))
+        bd = int(rng.choice([8, 10]))
+        n = int(rng.integers(1, 4))
+        h, w = int(rng.integers(k, 260)), int(rng.integers(k, 700))
+        pairs = [_pair(rng, h, w, bd) for _ in range(n)]
+        cfg = P.SsimConfig(bit_depth=bd, window=P.WindowSpec.gaussian(sigma, k=k, stride=s))
+        ref = torch.from_numpy(np.stack([p[0] for p in pairs])).cuda()
+        dist = torch.from_numpy(np.stack([p[1] for p in pairs])).cuda()
+        t = P.ssim_terms_batch(ref, dist, cfg)
+        got = np.stack([t.score.cpu().numpy(), t.l_mean.cpu().numpy(), t.cs_mean.cpu().numpy()], axis=1)
+        for i, (a, b) in enumerate(pairs):
+            want = oracle.ssim_terms(a, b, shape="gauss", k=k, sigma=sigma, stride=s, bit_depth=bd)
+            assert np.max(np.abs(got[i] - np.array(want))) < 1e-5, (k, sigma, s, bd, n, h, w, i)
