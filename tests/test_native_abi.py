@@ -169,3 +169,26 @@ def test_c_host_program_compiles_against_the_abi(tmp_path):
     exe = build_c_cli(tmp_path)
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 1 and "usage" in r.stderr
+
+
+def test_round2_entry_points_validate_without_gpu():
+    """The r2 C-ABI additions reject bad arguments before any launch (no GPU needed)."""
+    lib = nat.load_library()
+    vp = ctypes.c_void_p
+    assert lib.ssk_stats_from_sums(None, None, None, None, None, 4, 1.0, None, None) == nat.E_ARG
+    assert lib.ssk_stats_from_sums(vp(8), vp(8), vp(8), vp(8), vp(8), 4, 0.0, vp(8), None) == nat.E_ARG  # area
+    assert lib.ssk_term_maps(None, vp(8), vp(8), vp(8), vp(8), 4, 1.0, 1.0, vp(8), None) == nat.E_ARG
+    assert lib.ssk_divide(None, 4, 2.0, vp(8), None) == nat.E_ARG
+    m = nat.Maps(values=256, aux=None, dtype=nat.F64, n=1, h=4, w=5, row_pitch=5, frame_pitch=20,
+                 aux_row_pitch=0, aux_frame_pitch=0)
+    ws = lib.ssk_pairwise_workspace_bytes(ctypes.byref(m))
+    assert ws == 8  # 20 samples: a single subtree
+    out = vp(64)
+    assert lib.ssk_pairwise_sum(ctypes.byref(m), nat.PW_SQDEV, 0.0, 0.0, 0.0, None, out, vp(64), ws, None) == nat.E_ARG
+    assert lib.ssk_pairwise_sum(ctypes.byref(m), 99, 0.0, 0.0, 0.0, None, out, vp(64), ws, None) == nat.E_ARG
+    assert lib.ssk_pairwise_sum(ctypes.byref(m), nat.PW_LW, 0.0, 0.0, 0.0, None, out, vp(64), ws, None) == nat.E_ARG
+    assert lib.ssk_pairwise_sum(ctypes.byref(m), nat.PW_V, 0.0, 0.0, 0.0, None, out, vp(64), 0, None) == \
+        nat.E_WORKSPACE
+    big = nat.Maps(values=256, aux=None, dtype=nat.F64, n=2, h=1070, w=1910, row_pitch=1910,
+                   frame_pitch=1070 * 1910, aux_row_pitch=0, aux_frame_pitch=0)
+    assert lib.ssk_pairwise_workspace_bytes(ctypes.byref(big)) == 2 * (1 << 12) * 8  # depth-12 top tree
