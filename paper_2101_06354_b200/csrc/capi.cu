@@ -32,6 +32,13 @@ int gauss_persist_level() {
   }();
   return v;
 }
+int gauss_l0_classic() {
+  static const int v = [] {
+    const char* e = std::getenv("SSK_L0_CLASSIC");  // wide u8 frames on the classic kernel, 2 CTAs/SM (0 = persistent warp-specialised)
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
 int sm_count() {
   static int cached[64] = {0};
   int dev = 0;
@@ -248,6 +255,7 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
     a.shift = shift;
     a.c1 = (float)win->c1;
     a.c2 = (float)win->c2;
+    a.one = 1.0f;
     a.want = want;
     // x' = m * 2^-scale with |m| <= 2^(bd+scale) (per-tile shift anywhere in [0, L]): x'^2 is
     // exact in fp32 when m^2 fits 24 bits

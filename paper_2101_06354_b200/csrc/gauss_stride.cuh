@@ -12,7 +12,7 @@
 //            rows whose windows contain the row -- k/S FMAs per sample and moment instead
 //            of K1's k (the row -> anchor scatter is resolved at compile time from S).
 //   H pass : item = one anchor; k-tap horizontal filter of its V values (shared memory),
-//            then K1's epilogue (the same Sm / Dq / Su algebra, C2 carried by the filter).
+//            then K1's epilogue (the same sum / difference algebra, 2 C2 carried by the filter).
 // Two frames per CTA as packed fp32 pairs (FFMA2), K1's per-tile symmetric sample shift,
 // fp64 partial sums per (frame, CTA) in K1's [n][nseg][nstrips][3] layout.  Score-only:
 // map launches stay on K1, whose strided maps equal its dense maps at [::s, ::s] exactly.
@@ -105,45 +105,59 @@ __global__ void __launch_bounds__(SG_THREADS, 2) gauss_stride_kernel(const __gri
   };
   stage_rows(y0, y0 + NIN);
 
-  // per-tile symmetric shift (as K1): rounded mean of (x + y) / 2 over the tile's middle row
+  // per-tile symmetric shifts (as K1): rounded means of (x + y) / 2 and of x - y over the
+  // tile's middle row
+  __shared__ int s_dsum[SG_THREADS / 32][2];
   {
     const int r = min(((ar0 + ar1) / 2) * S + K / 2, a.h - 1);
     unsigned v0 = 0u, v1 = 0u;
+    int w0 = 0, w1 = 0;
     if (tid < TWI && cx0 + tid < a.w) {
       const long long off = (long long)r * a.row_pitch_b + (long long)(cx0 + tid) * ES;
-      if constexpr (ES == 1) {
-        v0 = (unsigned)a.ref[fo0 + off] + a.dist[fo0 + off];
-        v1 = (unsigned)a.ref[fo1 + off] + a.dist[fo1 + off];
-      } else {
-        v0 = (unsigned)*reinterpret_cast<const unsigned short*>(a.ref + fo0 + off) +
-             *reinterpret_cast<const unsigned short*>(a.dist + fo0 + off);
-        v1 = (unsigned)*reinterpret_cast<const unsigned short*>(a.ref + fo1 + off) +
-             *reinterpret_cast<const unsigned short*>(a.dist + fo1 + off);
-      }
+      const unsigned xr0 = raw_uint<TIN>(a.ref + fo0 + off), yd0 = raw_uint<TIN>(a.dist + fo0 + off);
+      const unsigned xr1 = raw_uint<TIN>(a.ref + fo1 + off), yd1 = raw_uint<TIN>(a.dist + fo1 + off);
+      v0 = xr0 + yd0;
+      v1 = xr1 + yd1;
+      w0 = (int)xr0 - (int)yd0;
+      w1 = (int)xr1 - (int)yd1;
     }
     v0 = __reduce_add_sync(0xffffffffu, v0);
     v1 = __reduce_add_sync(0xffffffffu, v1);
+    w0 = __reduce_add_sync(0xffffffffu, w0);
+    w1 = __reduce_add_sync(0xffffffffu, w1);
     if ((tid & 31) == 0) {
       s_tsum[tid >> 5][0] = v0;
       s_tsum[tid >> 5][1] = v1;
+      s_dsum[tid >> 5][0] = w0;
+      s_dsum[tid >> 5][1] = w1;
     }
   }
   __syncthreads();
   unsigned t0 = 0u, t1 = 0u;
+  int u0 = 0, u1 = 0;
 #pragma unroll
   for (int wi = 0; wi < SG_THREADS / 32; ++wi) {
     t0 += s_tsum[wi][0];
     t1 += s_tsum[wi][1];
+    u0 += s_dsum[wi][0];
+    u1 += s_dsum[wi][1];
   }
   const unsigned nsh = (unsigned)max(1, min(TWI, a.w - cx0));
   const float sc = a.conv_scale;
   const float cv0 = (float)((t0 + nsh) / (2u * nsh)) * sc, cv1 = (float)((t1 + nsh) / (2u * nsh)) * sc;
+  const int d0 = (int)(((unsigned)abs(u0) + nsh / 2u) / nsh), d1 = (int)(((unsigned)abs(u1) + nsh / 2u) / nsh);
+  const float dv0 = (float)(u0 < 0 ? -d0 : d0) * sc, dv1 = (float)(u1 < 0 ? -d1 : d1) * sc;
   const float base = -8388608.f * sc;
+  const float baseb = -(8388608.f + (float)SD_OFF) * sc;
   const u64 vbias = pk(base - cv0, base - cv1);
+  const u64 abias = pk(base - 2.f * cv0, base - 2.f * cv1);  // sum / difference form (gauss_ssim.cuh)
+  const u64 bbias = pk(baseb - dv0, baseb - dv1);
+  const u64 dshift = pk(dv0, dv1);
+  const u64 twoc1_2 = pk(2.f * a.c1, 2.f * a.c1), twoc2_2 = pk(2.f * a.c2, 2.f * a.c2);
   const u64 h2shift = pk(2.f * cv0, 2.f * cv1);
   const u64 scale2 = pk(sc, sc);
   const u64 c1_2 = pk(a.c1, a.c1), c2_2 = pk(a.c2, a.c2);
-  const u64 two2 = pk(2.f, 2.f), one2 = pk(1.f, 1.f), half2 = pk(0.5f, 0.5f), mhalf2 = pk(-0.5f, -0.5f);
+  const u64 two2 = pk(2.f, 2.f), one2 = pk(a.one, a.one), half2 = pk(0.5f, 0.5f), mhalf2 = pk(-0.5f, -0.5f);
   const bool exact_sq = a.exact_sq != 0;
   const bool full_terms = (a.want & (SSK_WANT_Q | SSK_WANT_L)) != 0;
   u64 w2[NH];
@@ -175,15 +189,29 @@ __global__ void __launch_bounds__(SG_THREADS, 2) gauss_stride_kernel(const __gri
 #pragma unroll
       for (int u = 0; u < NIN; ++u) {
         const unsigned char* rp = (u < wrap ? pa : pb) + u * 4 * RB;
+        u64 P[4];
+#if SSK_SD
+        {
+          const unsigned x0 = raw_uint<TIN>(rp), x1 = raw_uint<TIN>(rp + RB);
+          const unsigned y0 = raw_uint<TIN>(rp + 2 * RB), y1 = raw_uint<TIN>(rp + 3 * RB);
+          P[0] = fma2(pk(__uint_as_float(0x4B000000u + x0 + y0), __uint_as_float(0x4B000000u + x1 + y1)),
+                      scale2, abias);
+          P[1] = fma2(pk(__uint_as_float((0x4B000000u + SD_OFF) + x0 - y0),
+                         __uint_as_float((0x4B000000u + SD_OFF) + x1 - y1)),
+                      scale2, bbias);
+          P[2] = mul2(P[0], P[0]);
+          P[3] = mul2(P[1], P[1]);
+        }
+#else
         const u64 X = fma2(pk(raw_to_float<TIN>(rp), raw_to_float<TIN>(rp + RB)), scale2, vbias);
         const u64 Y = fma2(pk(raw_to_float<TIN>(rp + 2 * RB), raw_to_float<TIN>(rp + 3 * RB)), scale2, vbias);
-        u64 P[4];
         P[0] = X;
         P[1] = Y;
         if constexpr (ES == 1) P[2] = fma2(X, X, mul2(Y, Y));
         else if (exact_sq) P[2] = fma2(X, X, mul2(Y, Y));
         else P[2] = sumsq2(X, Y);
         P[3] = mul2(X, Y);
+#endif
 #pragma unroll
         for (int r = 0; r < G; ++r) {
           const int i = u - r * S;
@@ -207,11 +235,22 @@ __global__ void __launch_bounds__(SG_THREADS, 2) gauss_stride_kernel(const __gri
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         const u64* vr = vt + (m * G + r) * SG_THREADS + j * S;
-        u64 t = (m == 2) ? c2_2 : 0ull;  // E[x^2 + y^2] carries C2 (as K1)
+        u64 t = (m == 2) ? (SSK_SD ? twoc2_2 : c2_2) : 0ull;  // the squared-sum moment carries C2 (as K1)
 #pragma unroll
         for (int i = 0; i < K; ++i) t = fma2(w2[i < K - 1 - i ? i : K - 1 - i], vr[i], t);
         h[m] = t;
       }
+#if SSK_SD
+      u64 cs, l, q;
+      if (full_terms) {
+        sd_terms<true>(h[0], h[1], h[2], h[3], 2.f * a.c2, h2shift, dshift, twoc1_2, cs, l, q);
+        fq = fma2(q, one2, fq);
+        fl = fma2(l, one2, fl);
+      } else {
+        sd_terms<false>(h[0], h[1], h[2], h[3], 2.f * a.c2, h2shift, dshift, twoc1_2, cs, l, q);
+      }
+      fc = fma2(cs, one2, fc);
+#else
       const u64 m1 = h[0], m2 = h[1];
       const u64 nm2 = m2 ^ 0x8000000080000000ull;
       const u64 Sm = add2(m1, m2);
@@ -228,6 +267,7 @@ __global__ void __launch_bounds__(SG_THREADS, 2) gauss_stride_kernel(const __gri
         fq = fma2(mul2(l, cs), one2, fq);
         fl = fma2(l, one2, fl);
       }
+#endif
     }
   }
 
@@ -273,11 +313,12 @@ int launch_stride_k(const GaussArgs& a, dim3 grid, cudaStream_t st) {
 template <typename TIN, int S>
 int launch_stride_t(const GaussArgs& a, dim3 grid, int k, cudaStream_t st) {
   switch (k) {
+    case 11: return launch_stride_k<11, TIN, S>(a, grid, st);
+#ifndef SSK_K11_ONLY  // (A/B builds: only the 11-tap kernels, a quarter of the compile time)
     case 3: return launch_stride_k<3, TIN, S>(a, grid, st);
     case 5: return launch_stride_k<5, TIN, S>(a, grid, st);
     case 7: return launch_stride_k<7, TIN, S>(a, grid, st);
     case 9: return launch_stride_k<9, TIN, S>(a, grid, st);
-    case 11: return launch_stride_k<11, TIN, S>(a, grid, st);
     case 13: return launch_stride_k<13, TIN, S>(a, grid, st);
     case 15: return launch_stride_k<15, TIN, S>(a, grid, st);
     case 17: return launch_stride_k<17, TIN, S>(a, grid, st);
@@ -288,6 +329,7 @@ int launch_stride_t(const GaussArgs& a, dim3 grid, int k, cudaStream_t st) {
     case 27: return launch_stride_k<27, TIN, S>(a, grid, st);
     case 29: return launch_stride_k<29, TIN, S>(a, grid, st);
     case 31: return launch_stride_k<31, TIN, S>(a, grid, st);
+#endif
     default: return SSK_E_SHAPE;
   }
 }

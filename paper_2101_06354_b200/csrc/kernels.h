@@ -22,6 +22,8 @@ struct GaussArgs {
   float conv_scale, conv_bias;  // shifted sample = fma(raw_or_biased, scale, bias)
   float shift;                // added back to the means
   float c1, c2;
+  float one;                  // 1.0f, opaque to ptxas: sum += v * one stays an FFMA2 whose product is never
+                              // contracted with the multiply that formed v (rounding independent of `want`)
   int want;
   int exact_sq;               // shifted samples square exactly in fp32 (symmetric fast products)
   int vcols;                  // V-pass columns per CTA: 128, or 256 (wide warp-specialised u8 kernel)

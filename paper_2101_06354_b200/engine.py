@@ -192,6 +192,7 @@ def ssim(pair: DevicePair, window, c1: float, c2: float, want: int, stream=None)
 # (measured on 64 x 1080p: 1.007 -> 0.983 ms per MS-SSIM step).  Per-frame results
 # do not depend on the split (segmentation depends on the frame geometry only).
 SPLIT_MIN_FRAMES = 32
+_DEFAULT_PARTS = int(os.environ.get("SSK_MSSSIM_PARTS", "2"))  # A/B switch: sub-batches of a large batch
 _SIDE_STREAMS: dict = {}
 
 
@@ -199,10 +200,12 @@ def _side_streams(device, count: int):
     torch = nat.torch_mod()
     key = device.index
     have = _SIDE_STREAMS.get(key, [])
-    prio = int(os.environ.get("SSK_SIDE_PRIORITY", "1"))
+    prio = int(os.environ.get("SSK_SIDE_PRIORITY", "0"))
     while len(have) < count:
         # optionally the first half's stream at high priority: its coarse levels get CTA
-        # slots ahead of the second half's level-0 tiles as SMs free up
+        # slots ahead of the second half's level-0 tiles as SMs free up (helped the persistent
+        # level-0 kernel, 0.897 -> 0.892 ms; with the classic two-CTAs-per-SM level-0 kernel
+        # equal priorities measure 0.866 vs 0.911 ms per step, so it is off by default)
         have.append(torch.cuda.Stream(device=device, priority=-1 if (prio and not have) else 0))
     _SIDE_STREAMS[key] = have
     return have[:count]
@@ -241,7 +244,7 @@ def msssim_levels(pair: DevicePair, window, c1: float, c2: float, levels: int,
                             nat.stream_handle(st))
         nat.raise_for(rc, "msssim")
 
-    parts = split if split is not None else (2 if n >= SPLIT_MIN_FRAMES else 1)
+    parts = split if split is not None else (_DEFAULT_PARTS if n >= SPLIT_MIN_FRAMES else 1)
     parts = max(1, min(int(parts), n))
     if parts == 1:
         run(pair, 0, stream)

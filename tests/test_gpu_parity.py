@@ -688,6 +688,7 @@ def _adversarial_pairs():
     yy, xx = np.mgrid[0:h, 0:w]
     grad = ((xx * 255) // (w - 1)).astype(np.uint8)
     check = (((yy // 4 + xx // 4) % 2) * 255).astype(np.uint8)
+    tex = np.random.default_rng(5).integers(0, 256, (h, w))
     return {
         "flat_equal": (np.full((h, w), 77, np.uint8), np.full((h, w), 77, np.uint8)),
         "flat_extremes": (np.zeros((h, w), np.uint8), np.full((h, w), 255, np.uint8)),
@@ -695,6 +696,12 @@ def _adversarial_pairs():
         "gradient_plus_one": (grad, np.clip(grad.astype(int) + 1, 0, 255).astype(np.uint8)),
         "identical_texture": (check, check.copy()),
         "saturated_vs_texture": (np.full((h, w), 255, np.uint8), check),
+        # large flat ref/dist offsets: Var(x - y) = E[b^2] - E[b]^2 would cancel without the
+        # tile's difference shift d (sum / difference form of the score path); with opposite
+        # offsets in the two halves of every tile d cannot follow both
+        "offset_bright_vs_dark": ((tex // 4 + 180).astype(np.uint8), (tex // 4).astype(np.uint8)),
+        "offset_opposite_halves": (np.where(xx < w // 2, tex // 2 + 60, tex // 2).astype(np.uint8),
+                                   np.where(xx < w // 2, tex // 2, tex // 2 + 60).astype(np.uint8)),
     }
 
 
@@ -702,7 +709,7 @@ def _adversarial_pairs():
 def test_gaussian_adversarial_inputs_vs_oracle(cuda, oracle, name):
     """Flat windows (sigma ~ 0), extreme contrasts, exact identity and a near-flat gradient far
     from mid-gray through the fused Gaussian path (per-tile sample shift, C2 carried by the
-    filter, Sm / Dq / Su epilogue, fp32 tile sums): maps within 1e-4, scores within 1e-5 of
+    filter, sum / difference epilogue, fp32 tile sums): maps within 1e-4, scores within 1e-5 of
     the float64 oracle; MS-SSIM as well.  (With the fixed L/2 shift the gradient case was
     1.4e-4 off in cs and the shifted luminance form 3e-4 off in l.)"""
     a, b = _adversarial_pairs()[name]

@@ -213,6 +213,53 @@ def test_ssim3d_shard_halo_bounds():
         P.shard_with_halo(10, 0, 2, 0)
 
 
+def test_sum_difference_epilogue_algebra_matches_ssim_terms():
+    """The 4-moment Gaussian score path (csrc/gauss_ssim.cuh, sd_terms) filters a = x + y - 2c,
+    b = x - y - d and their squares: with Sm = E[a], Dm = E[b], Var(a) = s1^2 + s2^2 + 2 s12 and
+    Var(b) = s1^2 + s2^2 - 2 s12,
+        cs = (Var(a) - Var(b) + 2 C2) / (Var(a) + Var(b) + 2 C2),
+        l  = (Su^2 - Dt^2 + 2 C1) / (Su^2 + Dt^2 + 2 C1),  Su = Sm + 2c, Dt = Dm + d.
+    In float64 this must reproduce src/ssim.py:34-45 term for term; in float32 Var(b) must not
+    cancel when ref and dist differ by a large flat offset once b carries the tile shift d
+    (flat 0 vs flat 255 was 6.7e-5 off in cs with d = 0)."""
+    rng = np.random.default_rng(12)
+    c1, c2 = 6.5025, 58.5225
+    mu1, mu2 = rng.uniform(0, 255, 1000), rng.uniform(0, 255, 1000)
+    var1, var2 = rng.uniform(0, 500, 1000), rng.uniform(0, 500, 1000)
+    cov = rng.uniform(-1, 1, 1000) * np.sqrt(var1 * var2)
+    c, d = np.round((mu1 + mu2) / 2), np.round(mu1 - mu2)  # the tile shifts (any values work)
+    sm, dm = mu1 + mu2 - 2 * c, mu1 - mu2 - d
+    ea = var1 + var2 + 2 * cov + sm * sm + 2 * c2  # E[a^2] + 2 C2 (the filter carries 2 C2)
+    eb = var1 + var2 - 2 * cov + dm * dm           # E[b^2]
+    va, vb = ea - sm * sm, eb - dm * dm
+    cs_new = (va - vb) / (va + vb)
+    su, dt = sm + 2 * c, dm + d
+    h = su * su + 2 * c1
+    l_new = (h - dt * dt) / (h + dt * dt)
+    l_ref = (2 * mu1 * mu2 + c1) / (mu1 ** 2 + mu2 ** 2 + c1)
+    cs_ref = (2 * cov + c2) / (var1 + var2 + c2)
+    assert np.max(np.abs(l_new - l_ref)) < 1e-12 and np.max(np.abs(cs_new - cs_ref)) < 1e-12
+    # float32, flat 0 vs flat 255 through 11 fp32 taps: without d the filtered E[b^2] and
+    # E[b]^2 (65025 each) cancel to a residue of the tap-sum rounding; with d = -255 both are 0
+    f = np.float32
+    g = np.exp(-((np.arange(11) - 5.0) ** 2) / (2 * 1.5 ** 2))
+    taps = (g / g.sum()).astype(f)
+
+    def filt(v):
+        acc = f(0.0)
+        for t in taps:
+            acc = f(acc + f(t * f(v)))
+        return acc
+
+    for d32, tol in ((0.0, None), (-255.0, 0.0)):
+        b = f(-255.0 - d32)
+        vb32 = f(filt(b * b) - f(filt(b) * filt(b)))
+        if tol is not None:
+            assert abs(float(vb32)) <= tol
+        else:
+            assert abs(float(vb32)) < 0.1  # the residue the shift removes (vs 2 C2 = 117)
+
+
 def test_gaussian_epilogue_algebra_matches_ssim_terms():
     """The fused Gaussian epilogue (csrc/gauss_ssim.cuh, hpass) forms every term from the
     symmetric Sm = m1 + m2, Dq = (m1 - m2)^2 and Su = Sm + 2s of the shifted means
