@@ -514,7 +514,7 @@ def run_b200(args) -> None:
     achieved = flops / (kernel_ms * 1e-3) / 1e12
     peak = ctypes_probe(lib, 2.0)
     roofline = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": committed_traffic(), "kernel": "gauss_ws_persist_kernel<11, u8, 4, 256> (level-0 score launch over the 64-frame batch; the MS-SSIM step runs the same kernel with the fused level-1 stores)",
+                "traffic": committed_traffic(), "kernel": "gauss_levels_kernel<11, u8, 4, classic, 256> (level-0 score launch over the 64-frame batch, wide strips, 2 CTAs/SM; the MS-SSIM step runs the same kernel with the fused level-1 stores)",
                 "kernel_ms": kernel_ms, "flops_per_launch": flops,
                 "peak_source": "measured in-run: FFMA probe (ssk_probe_fp32_tflops, 2 s sustained); "
                                "MEASURED_PEAKS.json has no FP32 entry",

@@ -32,6 +32,13 @@ int gauss_persist_level() {
   }();
   return v;
 }
+int gauss_narrow_ws() {
+  static const int v = [] {
+    const char* e = std::getenv("SSK_NARROW_WS");  // 1 = warp-specialised kernel for 128-column strips
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
 int gauss_l0_classic() {
   static const int v = [] {
     const char* e = std::getenv("SSK_L0_CLASSIC");  // wide u8 frames on the classic kernel, 2 CTAs/SM (0 = persistent warp-specialised)

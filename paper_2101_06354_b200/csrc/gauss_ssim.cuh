@@ -1043,7 +1043,8 @@ int launch_ws(const GaussArgs& a, dim3 grid, cudaStream_t st) {
 
 template <int K, typename TIN>
 int launch_levels_one(const GaussLevels& p, dim3 grid, cudaStream_t st);
-int gauss_l0_classic();                       // capi.cu: SSK_L0_CLASSIC switch (default 0)
+int gauss_l0_classic();                       // capi.cu: SSK_L0_CLASSIC switch (default 1)
+int gauss_narrow_ws();                        // capi.cu: SSK_NARROW_WS switch (default 0)
 
 template <int K, typename TIN, int NM>
 int launch_nm(const GaussArgs& a, dim3 grid, cudaStream_t st) {
@@ -1068,7 +1069,9 @@ int launch_nm(const GaussArgs& a, dim3 grid, cudaStream_t st) {
     if constexpr (sizeof(TIN) <= 2 && 256 - (K - 1) >= 16) return launch_ws<K, TIN, NM, 256>(a, grid, st);
     return SSK_E_ARG;
   }
-  if (NM == 4 && !maps && gauss_ws_enabled()) return launch_ws<K, TIN, NM, GS_THREADS>(a, grid, st);
+  // 128-column strips: the classic kernel (4 CTAs/SM) measures ~5 % faster than the
+  // warp-specialised one since the sum / difference epilogue (SSK_NARROW_WS=1 restores it)
+  if (NM == 4 && !maps && gauss_ws_enabled() && gauss_narrow_ws()) return launch_ws<K, TIN, NM, GS_THREADS>(a, grid, st);
   auto fn = gauss_pair_kernel<K, TIN, NM>;
   const size_t smem = smem_bytes<K, TIN, NM, GS_THREADS, false>();
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)

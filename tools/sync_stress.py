@@ -106,8 +106,13 @@ def main() -> int:
         from paper_2101_06354_b200.csrc import build
 
         build.build(stress=True)
-    runs = [("production", {}), ("stress", {}), ("stress", {}), ("stress", {"SSK_PERSIST_CTAS": "1"}),
-            ("stress", {"SSK_PERSIST_CTAS": "3"}), ("stress", {"SSK_PERSIST_CTAS": "37"}), ("stress", {})]
+    # the default wide-u8 kernel is the classic one (two CTAs per SM); SSK_L0_CLASSIC=0 / SSK_NARROW_WS=1
+    # bring the warp-specialised kernels back -- the same arithmetic per item, so their outputs must equal
+    # the production build's bit for bit as well
+    ws = {"SSK_L0_CLASSIC": "0", "SSK_NARROW_WS": "1"}
+    runs = [("production", {}), ("stress", {}), ("stress", {}), ("stress", dict(ws)),
+            ("stress", dict(ws, SSK_PERSIST_CTAS="1")), ("stress", dict(ws, SSK_PERSIST_CTAS="3")),
+            ("stress", dict(ws, SSK_PERSIST_CTAS="37")), ("stress", {}), ("production", dict(ws))]
     results = []
     with tempfile.TemporaryDirectory() as td:
         for i, (lib, extra) in enumerate(runs):
