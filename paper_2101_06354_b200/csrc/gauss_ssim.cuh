@@ -224,7 +224,7 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
 // L1 = false compiles the fused pyramid-level-1 stores out (score-only persistent launches)
 template <int K, typename TIN, int NM, bool WS, int VC, bool PERSIST = false, bool MAPS = true, bool L1 = true>
 __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0, const int seg0, const int pair0,
-                                           const int nstrips, const int nseg) {
+                                           const int nstrips, const int nseg, const float (&taps)[32]) {
   constexpr int VP = vp_of(VC);
   constexpr int TW = tw_of(K, VC);
   constexpr int TWI = TW + K - 1;
@@ -243,7 +243,12 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* raw = smem;                        // [RR][4][RB]
   unsigned char* vbuf0 = smem + RR * 4 * RB;        // [WS ? 2 : 1][NM][G][VP]
+#ifndef SSK_TAPS_SMEM
+#define SSK_TAPS_SMEM 0
+#endif
+#if SSK_TAPS_SMEM
   __shared__ float s_taps[32];
+#endif
   __shared__ double s_red[(2 * VC / 32) * 6];
 
   // Warp-specialised kernels: logical thread ids swap the CTA's halves, so the producers
@@ -286,18 +291,48 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
   // and a ring-slot wrap (was a division / modulo chain per 16-byte item)
   constexpr int IPR = 4 * NCH;  // 16-byte items per input row (4 images)
   constexpr int RPP = VC / IPR;  // rows per pass (when IPR divides VC)
+  // Running-pointer mode (r2): a tile's rows are staged strictly in order (its first G + K - 1
+  // rows, then G more per chunk), so a thread's source pointer, row and ring slot simply run on
+  // from call to call; the first call of a tile (r_lo == y0) derives them.  Per chunk that is
+  // two copies and a handful of adds per thread -- the item loop spent ~90 instructions per
+  // chunk and thread on 64-bit row-address IMADs and a modulo (7 % of the kernel's stall
+  // samples sat on those IMADs, which share the FMA pipe with the filter).
+#ifndef SSK_STAGE_RUNNING
+#define SSK_STAGE_RUNNING 1
+#endif
+  const unsigned char* st_src = nullptr;
+  int st_row = 0, st_slot = 0;
   auto stage_rows = [&](int r_lo, int r_hi) {
     r_hi = min(r_hi, in_end);
-    // Measured (tools/ab_libs.sh, 64 x 1080p): the strength-reduced loop speeds up the
-    // score-only warp-specialised launch (0.667 -> 0.657 ms) but slows the MS-SSIM step
-    // when the producers also write the fused pyramid level 1 (0.912 -> 0.918 ms) and in
-    // the classic kernel (coarse levels, +0.005 ms): it runs only where it wins.
 #ifdef SSK_STAGE_GENERIC
     constexpr bool generic_stage = true;  // A/B build: the item loop everywhere
+    constexpr bool running_stage = false;
 #else
-    constexpr bool generic_stage = VC % IPR != 0 || !WS || L1;
+    constexpr bool running_stage = SSK_STAGE_RUNNING && VC % IPR == 0;
+    // (round-2 first pass, kept for SSK_STAGE_RUNNING=0: the per-call strength-reduced loop
+    // won only in the score-only warp-specialised launch)
+    constexpr bool generic_stage = !running_stage && (VC % IPR != 0 || !WS || L1);
 #endif
-    if constexpr (generic_stage) {  // generic item loop
+    if constexpr (running_stage) {
+      const int im = (tid % IPR) / NCH, q = tid % NCH;
+      int valid = row_bytes_left - q * 16;
+      valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
+      const long long pitch = a.row_pitch_b;
+      if (r_lo == y0) {  // first rows of a tile (uniform branch)
+        st_row = y0 + tid / IPR;
+        st_slot = tid / IPR;
+        st_src = ((im & 2) ? a.dist : a.ref) + ((im & 1) ? fo1 : fo0) + (valid ? (long long)c0 * ES + q * 16 : 0) +
+                 (long long)st_row * pitch;
+      }
+      unsigned char* dst = raw + im * RB + q * 16;
+      for (; st_row < r_hi; st_row += RPP) {
+        cp_async16(dst + st_slot * 4 * RB, st_src, valid);
+        st_src += RPP * pitch;
+        st_slot += RPP;
+        if (st_slot >= RR) st_slot -= RR;
+      }
+      cp_async_commit();
+    } else if constexpr (generic_stage) {  // generic item loop
       const int total = (r_hi - r_lo) * IPR;
       for (int i = tid; i < total; i += VC) {
         const int rr = i / IPR;
@@ -314,7 +349,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
         cp_async16(raw + (((row - y0) % RR) * 4 + im) * RB + off, src, valid);
       }
       cp_async_commit();
-    } else {  // strength-reduced loop
+    } else {  // strength-reduced loop, re-derived per call
       const int im = (tid % IPR) / NCH, q = tid % NCH;
       int valid = row_bytes_left - q * 16;
       valid = valid < 0 ? 0 : (valid > 16 ? 16 : valid);
@@ -335,11 +370,21 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
   };
 
   if (tid < VC) stage_rows(y0, y0 + G + K - 1);  // (persistent CTAs: their first tile)
+#if SSK_TAPS_SMEM
   if (tid < 32) s_taps[tid] = a.taps[tid];
   __syncthreads();
   u64 w2[NH];
 #pragma unroll
   for (int i = 0; i < NH; ++i) w2[i] = pk(s_taps[i], s_taps[i]);
+#else
+  // taps straight from the kernel arguments at a fixed offset (constant bank -> uniform
+  // registers; the multi-level launch reads its first level's, every level has the same
+  // window): through shared memory ptxas kept a third of them in vector registers, and an
+  // FFMA2 with a register-broadcast weight issues at 2.42 cycles instead of 2.04 (tools/ubench)
+  u64 w2[NH];
+#pragma unroll
+  for (int i = 0; i < NH; ++i) w2[i] = pk(taps[i], taps[i]);
+#endif
 
   const u64 scale2 = pk(a.conv_scale, a.conv_scale);
   const u64 bias2 = pk(a.conv_bias, a.conv_bias);
@@ -965,12 +1010,12 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
 
 template <int K, typename TIN, int NM>
 __global__ void __launch_bounds__(GS_THREADS, GS_MINB) gauss_pair_kernel(const __grid_constant__ GaussArgs a) {
-  gauss_body<K, TIN, NM, false, GS_THREADS>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.x, gridDim.y);
+  gauss_body<K, TIN, NM, false, GS_THREADS>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.x, gridDim.y, a.taps);
 }
 
 template <int K, typename TIN, int NM, int VC>
 __global__ void __launch_bounds__(2 * VC, VC == 128 ? 2 : 1) gauss_ws_kernel(const __grid_constant__ GaussArgs a) {
-  gauss_body<K, TIN, NM, true, VC>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.x, gridDim.y);
+  gauss_body<K, TIN, NM, true, VC>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.x, gridDim.y, a.taps);
 }
 
 // Persistent variant (one CTA per SM walking tiles blockIdx.x, + gridDim.x, ...)
@@ -978,7 +1023,7 @@ template <int K, typename TIN, int NM, int VC, bool L1>
 __global__ void __launch_bounds__(2 * VC, 1)
     gauss_ws_persist_kernel(const __grid_constant__ GaussArgs a, const int nstrips, const int nseg) {
   // (the map branch stays compiled in: measured faster here than the MAPS = false build)
-  gauss_body<K, TIN, NM, true, VC, true, true, L1>(a, 0, 0, 0, nstrips, nseg);
+  gauss_body<K, TIN, NM, true, VC, true, true, L1>(a, 0, 0, 0, nstrips, nseg, a.taps);
 }
 
 // All pyramid levels of one sample type in one launch: blockIdx.x enumerates the
@@ -995,7 +1040,7 @@ __global__ void __launch_bounds__(WS ? 2 * VC : VC, WS ? 2 : (VC == 256 ? 2 : 4)
   const int ns = p.nstrips[lv];
   const int ntiles = ns * p.nseg[lv];
   const int pair = local / ntiles, tile = local - pair * ntiles;
-  gauss_body<K, TIN, NM, WS, VC, false, false>(p.lv[lv], tile % ns, tile / ns, pair, ns, p.nseg[lv]);
+  gauss_body<K, TIN, NM, WS, VC, false, false>(p.lv[lv], tile % ns, tile / ns, pair, ns, p.nseg[lv], p.lv[0].taps);
 }
 
 template <int K, typename TIN, int NM, int VC = GS_THREADS, bool WS = true>
