@@ -638,11 +638,51 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
     const int xb = c0 >> 1, xe = min((last_strip ? a.w : c0 + TW) >> 1, a.l1_w);
     const int nx = xe - xb, ny = ye - yb;
     if (nx <= 0 || ny <= 0) return;
+    static_assert(RR % 2 == 0 && (TW + K - 1) / 2 <= 128, "level-1 item mapping");
+#ifndef SSK_L1_WIDE
+#define SSK_L1_WIDE 1
+#endif
+#if SSK_L1_WIDE
+    // 8 level-1 samples per item and image (r2): two 16-byte shared loads (rows 2y, 2y+1),
+    // byte-pair sums on packed 16-bit lanes, one 16-byte store (xb is a multiple of 8).
+    // Item = (level-1 row, octet of columns, side): thread t < 128 owns row t / 32 (+ 4 per
+    // pass), octet t % 16 and the side (ref / dist) of its half-warp, both frames -- a chunk's
+    // four level-1 rows are one pass of warps 0-3 at half the instructions per sample of the
+    // 4-sample items (35 -> ~20 us per 32-pair launch); warps 4-7 go straight to the V pass.
+    // RR is even, so row 2y+1 sits in slot s0 + 1.
+    const int no = (nx + 7) >> 3;
+    const int oct = tid & 15, side = (tid >> 4) & 1;
+    for (int r = tid >> 5; r < ny && oct < no && tid < 128; r += 4) {
+      const int yy = yb + r, x8 = xb + 8 * oct;
+      const int col = 2 * x8 - c0;
+      const int s0 = (2 * yy - y0) % RR, s1 = s0 + 1;
+      const int nvalid = min(8, xe - x8);
+#pragma unroll
+      for (int fi = 0; fi < 2; ++fi) {
+        const int im = 2 * side + fi;
+        if (fi && !has1) continue;
+        const uint4 a0 = *reinterpret_cast<const uint4*>(raw + (s0 * 4 + im) * RB + col);
+        const uint4 a1 = *reinterpret_cast<const uint4*>(raw + (s1 * 4 + im) * RB + col);
+        // [b0 b1 b2 b3] -> 16-bit lanes (b0 + b1, b2 + b3); four bytes add without carry
+        auto quad = [](unsigned u, unsigned v) {
+          return (u & 0x00FF00FFu) + ((u >> 8) & 0x00FF00FFu) + (v & 0x00FF00FFu) + ((v >> 8) & 0x00FF00FFu);
+        };
+        const uint4 o = make_uint4(quad(a0.x, a1.x), quad(a0.y, a1.y), quad(a0.z, a1.z), quad(a0.w, a1.w));
+        unsigned short* dst = (side ? a.l1_dist : a.l1_ref) + (long long)(fi ? f1 : f0) * a.l1_fp +
+                              (long long)yy * a.l1_rp + x8;
+        if (nvalid == 8) {
+          *reinterpret_cast<uint4*>(dst) = o;
+        } else {
+          const unsigned w4[4] = {o.x, o.y, o.z, o.w};
+          for (int j = 0; j < nvalid; ++j) dst[j] = (unsigned short)(w4[j >> 1] >> (16 * (j & 1)));
+        }
+      }
+    }
+#else
     // 4 level-1 samples per item: two 8-byte shared loads per image (rows 2y, 2y+1),
     // pairwise byte sums on packed 16-bit lanes, one 8-byte store (xb is a multiple of 4).
     // Item (row, quad) = (tid / 32 + k * VC / 32, tid % 32): at most 32 quads per row
     // (nx <= (TW + K - 1) / 2), so no division; RR is even, so row 2y+1 sits in slot s0 + 1.
-    static_assert(RR % 2 == 0 && (TW + K - 1) / 2 <= 128, "level-1 item mapping");
     const int nq = (nx + 3) >> 2;
     const int q = tid & 31;
     for (int r = tid >> 5; r < ny && q < nq; r += VC >> 5) {
@@ -671,6 +711,7 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
         }
       }
     }
+#endif
   };
 
   // ---------------- H pass + epilogue: thread = (row, 8 columns) ----------------
@@ -1138,6 +1179,7 @@ int launch_levels_one(const GaussLevels& p, dim3 grid, cudaStream_t st) {
   // (small tiles, 3-4 CTAs/SM); SSK_GAUSS_WS=2 forces the warp-specialised variant
   if constexpr (K <= 17) {
     if (p.lv[0].vcols == 256) {  // wide strips (240 outputs), 2 CTAs of 256 threads per SM
+      // (a separate build without the fused level-1 stores measured the same: 0.5812 ms)
       auto fw = gauss_levels_kernel<K, TIN, 4, false, 256>;
       const size_t smem = smem_bytes<K, TIN, 4, 256, false>();
       if (cudaFuncSetAttribute(fw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
