@@ -264,13 +264,13 @@ import paper_2101_06354_b200 as P
 rng = np.random.default_rng(77)
 cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
 out = {}
-for name, (n, h, w) in {"wide": (41, 512, 600), "narrow": (5, 70, 90)}.items():
+for name, (n, h, w) in {"wide": (41, 512, 600), "narrow": (5, 70, 90), "odd": (3, 517, 963)}.items():
     a = rng.integers(0, 256, (n, h, w)).astype(np.uint8)
     b = np.clip(a.astype(int) + rng.integers(-30, 31, a.shape), 0, 255).astype(np.uint8)
     ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
     t = P.ssim_terms_batch(ta, tb, cfg)
     out[name + "_terms"] = torch.stack([t.score, t.l_mean, t.cs_mean], 1).cpu().numpy()
-    out[name + "_ms"] = P.msssim_batch(ta, tb, cfg, P.MultiscaleSpec.product(2)).cpu().numpy()
+    out[name + "_ms"] = P.msssim_batch(ta, tb, cfg, P.MultiscaleSpec.product(2 if h < 100 else 3)).cpu().numpy()
 np.savez(sys.argv[1], **out)
 """
 
@@ -280,22 +280,26 @@ def test_warp_specialised_kernels_match_the_default_kernels_bit_for_bit(cuda, tm
     classic 128-column kernel; SSK_L0_CLASSIC=0 / SSK_NARROW_WS=1 select the persistent and the
     narrow warp-specialised kernels (read once per process, hence subprocesses).  The
     arithmetic per item is the same code, so scores, terms and MS-SSIM (fused level 1) must be
-    bit-identical -- 41 wide frames give the persistent CTAs several tiles each."""
+    bit-identical -- 41 wide frames give the persistent CTAs several tiles each.  A third run
+    with SSK_FUSED_L1=0 builds pyramid level 1 in the separate pyramid pass: the fused stores
+    (16-byte items, odd sizes, ragged last strip) must produce the same exact integers, hence
+    the same MS-SSIM bits."""
     import os
     import subprocess
     import sys
 
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     results = []
-    for i, extra in enumerate(({}, {"SSK_L0_CLASSIC": "0", "SSK_NARROW_WS": "1"})):
+    for i, extra in enumerate(({}, {"SSK_L0_CLASSIC": "0", "SSK_NARROW_WS": "1"}, {"SSK_FUSED_L1": "0"})):
         path = str(tmp_path / f"ws{i}.npz")
         env = dict(os.environ, PYTHONPATH=repo + os.pathsep + os.environ.get("PYTHONPATH", ""), **extra)
         r = subprocess.run([sys.executable, "-c", _WS_CASE, path], env=env, capture_output=True, text=True, cwd=repo)
         assert r.returncode == 0, r.stderr[-2000:]
         with np.load(path) as z:
             results.append({k: z[k] for k in z.files})
-    for k, v in results[0].items():
-        assert np.array_equal(v, results[1][k]), k
+    for other in results[1:]:
+        for k, v in results[0].items():
+            assert np.array_equal(v, other[k]), k
 
 
 @pytest.mark.parametrize("n", [2, 7, 40])
