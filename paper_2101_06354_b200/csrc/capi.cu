@@ -219,11 +219,12 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
     a.stride = s;
     // wide strips (256 V columns, 1 CTA/SM) for 8-bit frames under the warp-specialised
     // kernel: V-halo overhead 250/240 instead of 122/112 and fewer idle H threads
-    // (u16 -- the scaled pyramid level 1 of 8-bit input -- only with SSK_WIDE_U16=1:
-    // measured no faster than the classic multi-level launch, which saves a launch)
+    // (16-bit frames too since the classic kernel took over the wide strips, r2: 10-bit 1080p
+    // scores 101.7 k pairs/s on 256-column strips vs 91.8 k on 128-column ones; SSK_WIDE_U16=0
+    // restores the narrow strips)
     static const int wide_u16 = [] {
       const char* e = std::getenv("SSK_WIDE_U16");
-      return e ? std::atoi(e) : 0;
+      return e ? std::atoi(e) : 1;
     }();
     // coarse pyramid levels (u16 scaled sums): wide strips on the classic multi-level kernel
     static const int levels_wide = [] {
