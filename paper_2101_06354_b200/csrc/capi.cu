@@ -234,7 +234,18 @@ int plan_ssim(const ssk_planes* p, const ssk_window* win, int want, Plan& pl) {
     const bool coarse_wide = p->dtype == SSK_U16 && p->scale_log2 > 0 && levels_wide;
     const bool wide_ok = p->dtype == SSK_U8 || (p->dtype == SSK_U16 && (wide_u16 || coarse_wide));
     const bool maps = (want & (SSK_MAP_TERMS | SSK_MAP_STATS)) != 0;  // maps: classic kernel only
-    a.vcols = (gk::gauss_ws_level() >= 1 && wide_ok && !maps && k <= 17 && (a.wo >= 480 || coarse_wide)) ? 256 : 128;
+    static const int wide_min_wo = [] {  // narrowest output width that gets 256-column strips
+      const char* e = std::getenv("SSK_WIDE_MIN_WO");
+      return e ? std::atoi(e) : 480;
+    }();
+    // below that width: wide strips where they cover the row with no more V columns than
+    // narrow ones (one 240-column strip vs two or three of 112, or two vs four / five):
+    // 480 x 480 frames 0.113 -> 0.097 ms per 64 pairs, 352 x 288 0.177 -> 0.163 ms per 256
+    const int tw_w = gauss_tw(k, 256), tw_n = gauss_tw(k, 128);
+    const bool cols_ok = tw_w > 0 && tw_n > 0 &&
+                         (long long)((a.wo + tw_w - 1) / tw_w) * 256 <= (long long)((a.wo + tw_n - 1) / tw_n) * 128;
+    a.vcols = (gk::gauss_ws_level() >= 1 && wide_ok && !maps && k <= 17 &&
+               (a.wo >= wide_min_wo || cols_ok || coarse_wide)) ? 256 : 128;
     const int tw = gauss_tw(k, a.vcols);
     const int nstrips = (a.wo + tw - 1) / tw;
     // Segments depend on the frame geometry only (never on the batch size), so a
