@@ -9,28 +9,35 @@
 // with the normalised 1-D taps g/sum(g) (identical up to rounding;
 // tests/test_stats.py:126-129 pins separability).
 //
-// Blackwell design.  One CTA = 128 threads = a strip of TW output columns
-// (TW + K - 1 <= 128 input columns) of a segment of output rows, for TWO
-// frames at once: every value is carried as a packed fp32 pair (frame f,
-// frame f+1), so the whole filter runs on FFMA2 / FMUL2 / FADD2 -- two FMAs
-// per lane per issued instruction -- without any register shuffling (the
-// pairing is across frames, which share all addresses and weights).
-//   stage  : cp.async 16-B copies of G new input rows of the 4 images
-//            (ref/dist x 2 frames) into a ring of 2G+K-1 raw rows, one chunk
-//            ahead of the compute (double buffering), zero fill past the edge.
-//   V pass : thread = input column; converts samples exactly to fp32 (u8/u16
-//            via the 2^23-mantissa splice), subtracts a symmetric shift -- per
-//            tile, the rounded mean of (x + y) / 2 over the tile's middle row,
-//            for every sample type (keeps E[x^2]-E[x]^2 well conditioned in
-//            fp32 and preserves exact ref/dist symmetry),
-//            forms x, y, x^2, y^2, xy and gathers the
-//            K-tap vertical filter for G output rows (5*G packed accumulators).
-//   H pass : thread = (output row, 8 adjacent columns); K-tap horizontal filter
-//            from the shared-memory V rows, then the SSIM epilogue on packed
-//            pairs, optional map stores and per-frame fp64 partial sums.
-//   reduce : warp-shuffle + shared-memory block reduction into one fp64
-//            partial per (frame, CTA); a second tiny kernel folds the partials
-//            per frame in a fixed order (bit-reproducible, batch-independent).
+// Blackwell design.  One CTA = VC threads (256 for frames wide enough, else 128) = a strip
+// of TW output columns (TW + K - 1 <= VC input columns) of a segment of output rows, for TWO
+// frames at once: every value is carried as a packed fp32 pair (frame f, frame f+1), so the
+// whole filter runs on FFMA2 / FMUL2 / FADD2 -- two FMAs per lane per issued instruction --
+// without any register shuffling (the pairing is across frames, which share all addresses
+// and weights).  The kernel is issue-bound (an FFMA2 holds the issue port for both of its
+// cycles, tools/ubench/ffma2_forms.cu), so the design minimises instructions per output.
+//   stage  : cp.async 16-B copies of G new input rows of the 4 images (ref/dist x 2 frames)
+//            into a ring of raw rows, one chunk ahead of the compute, zero fill past the
+//            edge; each thread's source pointer / ring slot run on from chunk to chunk.
+//   V pass : thread = input column.  Score path (4 moments, sum / difference form): forms
+//            a = x + y - 2c and b = x - y - d exactly (8/16-bit samples: inside the 2^23
+//            integer -> float splice, one IADD3 and one FFMA2 each; c, d = the tile's rounded
+//            means of (x + y) / 2 and x - y over its middle row, symmetric in ref / dist, which
+//            keep E[a^2] - E[a]^2 and E[b^2] - E[b]^2 well conditioned in fp32), squares them
+//            and gathers the K-tap vertical filter for G output rows (4*G packed accumulators;
+//            taps in uniform registers).  Statistics maps (5 moments): x, y, x^2, y^2, xy.
+//   H pass : thread = (output row, 8 adjacent columns); K-tap horizontal filter from the
+//            shared-memory V rows (16-byte loads), then the SSIM epilogue on packed pairs
+//            (sd_terms: 15 FMA-pipe ops and 4 reciprocals per output pair), optional map
+//            stores and per-frame partial sums.
+//   reduce : warp-shuffle + shared-memory block reduction into one fp64 partial per
+//            (frame, CTA); a second tiny kernel folds the partials per frame in a fixed
+//            order (bit-reproducible, batch-independent).
+// Variants of the one body (gauss_body): the classic kernel (every thread runs V then H
+// behind two CTA barriers per chunk; 2 x 256 or 4 x 128 threads per SM -- the default), the
+// multi-level launch (tiles of several pyramid levels in one grid), and the warp-specialised
+// kernels (producer warps V, consumer warps H over a ring of V tiles behind named barriers;
+// persistent for wide u8 frames) kept as A/B alternatives (SSK_L0_CLASSIC=0, SSK_NARROW_WS=1).
 // Every output value is produced by the same operation sequence whatever the
 // stride, so strided grids equal dense[::s, ::s] bit-exactly
 // (tests/test_stats.py:274-285).
