@@ -258,6 +258,47 @@ def test_persistent_wide_kernel_multi_tile_ctas(cuda, rng):
     assert abs(got[40, 0] - P.ssim_score(a[40], b[40], cfg)) == 0.0
 
 
+def test_workspace_keeps_its_guards(cuda, rng, monkeypatch):
+    """Bounds evidence without compute-sanitizer (closed on this pool): every library call gets a
+    workspace of exactly the queried size carved out of the middle of a larger, pre-filled
+    buffer -- the pyramid levels (fused level-1 stores on ragged strips, 16-byte items; the
+    pyramid pass) and the per-CTA partial sums live there and must leave every guard byte on
+    both sides untouched, for odd geometries, strided scores and 10-bit frames."""
+    import torch
+    from paper_2101_06354_b200 import _native as nat
+
+    guard = 8192
+
+    class Guarded:
+        def __init__(self):
+            self.bufs = []
+
+        def get(self, nbytes, device, stream=None):
+            nb = (max(int(nbytes), 256) + 255) // 256 * 256
+            buf = torch.full((nb + 2 * guard,), 0xA5, dtype=torch.uint8, device=device)
+            self.bufs.append(buf)
+            return buf[guard:guard + nb]
+
+    g = Guarded()
+    monkeypatch.setattr(nat, "WORKSPACE", g)
+    cfg = P.SsimConfig(window=P.WindowSpec.gaussian(1.5))
+    for n, h, w, levels in ((3, 517, 963, 4), (2, 140, 250, 2), (5, 97, 491, 3)):
+        a = rng.integers(0, 256, (n, h, w)).astype(np.uint8)
+        b = np.clip(a.astype(int) + rng.integers(-20, 21, a.shape), 0, 255).astype(np.uint8)
+        ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        P.msssim_batch(ta, tb, cfg, P.MultiscaleSpec.product(levels), with_ssim=True)
+        P.ssim_terms_batch(ta, tb, cfg)
+        P.ssim_terms_batch(ta, tb, P.SsimConfig(window=P.WindowSpec.gaussian(1.5, stride=3)))
+    a16 = rng.integers(0, 1024, (3, 200, 700)).astype(np.uint16)
+    b16 = np.clip(a16.astype(int) + rng.integers(-40, 41, a16.shape), 0, 1023).astype(np.uint16)
+    c10 = P.SsimConfig(bit_depth=10, window=P.WindowSpec.gaussian(1.5))
+    P.msssim_batch(torch.from_numpy(a16).cuda(), torch.from_numpy(b16).cuda(), c10, P.MultiscaleSpec.product(3))
+    torch.cuda.synchronize()
+    assert len(g.bufs) >= 10
+    for buf in g.bufs:
+        assert bool((buf[:guard] == 0xA5).all()) and bool((buf[-guard:] == 0xA5).all())
+
+
 _WS_CASE = r"""
 import sys, numpy as np, torch
 import paper_2101_06354_b200 as P
