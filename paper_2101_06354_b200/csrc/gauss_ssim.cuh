@@ -125,6 +125,19 @@ inline bool gauss_ws_enabled() { return gauss_ws_level() >= 1; }
 #endif
 __host__ __device__ constexpr int vp_of(int vc) { return SSK_H128 ? vc * 8 + 16 : vc * 8 + 8; }
 __host__ __device__ constexpr int tw_of(int k, int vc) { return ((vc - (k - 1)) / 16) * 16; }
+// Raw ring rows.  Warp-specialised kernels stage chunk c+1 while chunk c is read (2G + K - 1);
+// the classic kernel refills the G oldest rows right after its V pass, so the G + K - 1 rows of
+// a chunk suffice -- for 8-bit samples rounded up to whole groups of G rows (r2): a chunk then
+// reads whole groups, each contiguous, so every row's address is one of a few per-chunk group
+// bases plus an immediate (no per-row wrap select; 16-bit strips keep the exact ring, whose
+// extra rows would cost them a CTA per SM).
+#ifndef SSK_RING_GROUPS
+#define SSK_RING_GROUPS 1
+#endif
+__host__ __device__ constexpr bool ring_grouped(bool ws, int es) { return SSK_RING_GROUPS && !ws && es == 1; }
+__host__ __device__ constexpr int ring_rows(int k, bool ws, int es) {
+  return ws ? 2 * GS_G + k - 1 : (ring_grouped(ws, es) ? (GS_G + k - 1 + GS_G - 1) / GS_G * GS_G : GS_G + k - 1);
+}
 // V tiles in flight: 3, except wide 16-bit strips (their doubled raw ring leaves room for 2)
 __host__ __device__ constexpr int nbuf_of(int vc, int es) { return (vc == 256 && es > 1) ? 2 : GS_NBUF; }
 
@@ -241,7 +254,8 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
   // raw ring rows: the warp-specialised kernel stages chunk c+1 while chunk c is read
   // (2G + K - 1); the classic kernel refills the G oldest rows right after its V pass,
   // so the copy overlaps the H pass and the ring needs only the G + K - 1 rows of a chunk
-  constexpr int RR = WS ? 2 * G + K - 1 : G + K - 1;
+  constexpr int RR = ring_rows(K, WS, ES);
+  constexpr bool GROUPED = ring_grouped(WS, ES);
   constexpr int NH = (K + 1) / 2;
   constexpr int NP = 8 + K - 1;                     // V values read per H item
   static_assert(TWI <= VC, "strip wider than the CTA");
@@ -575,9 +589,22 @@ __device__ __forceinline__ void gauss_body(const GaussArgs& a, const int strip0,
       const int wrap = RR - s0;
       const unsigned char* pa = raw + s0 * 4 * RB + tid * ES;
       const unsigned char* pb = pa - RR * 4 * RB;
+      // grouped ring: the chunk's rows are groups g0, g0 + 1, ... (mod NG) of G rows each
+      constexpr int NG = RR / G;
+      const unsigned char* pg[GROUPED ? NG : 1];
+      if constexpr (GROUPED) {
+        const int g0 = c % NG;
+#pragma unroll
+        for (int k = 0; k < NG; ++k) {
+          const int gk = g0 + k < NG ? g0 + k : g0 + k - NG;
+          pg[k] = raw + gk * G * 4 * RB + tid * ES;
+        }
+      }
 #pragma unroll
       for (int u = 0; u < G + K - 1; ++u) {
-        const unsigned char* rp = (u < wrap ? pa : pb) + u * 4 * RB;
+        const unsigned char* rp;
+        if constexpr (GROUPED) rp = pg[u / G] + (u % G) * 4 * RB;
+        else rp = (u < wrap ? pa : pb) + u * 4 * RB;
         u64 P[NM];
         if constexpr (NM == 4 && SSK_SD && ES <= 2) {
           // x + y and x - y inside the 2^23 splice (one IADD3 each), then one exact FFMA2 each
@@ -1095,7 +1122,7 @@ template <int K, typename TIN, int NM, int VC = GS_THREADS, bool WS = true>
 inline size_t smem_bytes() {
   constexpr int TWI = tw_of(K, VC) + K - 1;
   constexpr int RB = ((TWI * (int)sizeof(TIN) + 15) / 16) * 16;
-  constexpr int RR = WS ? 2 * G + K - 1 : G + K - 1;
+  constexpr int RR = ring_rows(K, WS, (int)sizeof(TIN));
   return (size_t)RR * 4 * RB + (size_t)NM * G * vp_of(VC);
 }
 
